@@ -1,0 +1,325 @@
+"""oracle/selector_ref.py -- TEST INFRASTRUCTURE ONLY (parity oracle, never on the product path).
+
+A plain, pure-Python-int re-implementation of Vortex's two-stage method as DESIGN.md
+section 3 specifies it for sm_100a, written step by step in the paper's order:
+
+  offline  (sample-free strategy table, "vx_plan"):
+      Alg. 2 "GenerateCandidatesForLayer" (Sec. 5.1):
+        L0: InitCands -> FilterByISA
+        L>=1: InitCands -> FilterByMultiples(prev) + map
+      hardware limits from GetHardwareInfo
+  runtime  (shape-dependent selection, "vx_plan_select"):
+      Eq. 2  T_temporal = T_Load + (sizeof(TemporalLoop)-1)*max(T_Load, Cost_{L-1})
+                          + Cost_{L-1} + T_Store
+      Eq. 3  F_parallel = ceil(sizeof(ParallelLoop) / |HardwareUnit|)
+      Eq. 4  Cost_L = F_parallel * T_temporal
+      Eq. 1  c* = argmin_{s in S} Cost(s, L)
+      "at runtime ... analytical cost models ... select the most suitable micro-kernel
+       candidates ... compute ... grid configurations"
+
+Every reading the paper leaves open (lattice, window, split-K, persistence, tie-break,
+integer units) is listed in DESIGN.md "Readings" and cited inline as R<n>.
+
+Inputs are data only: the device descriptor (captured from the B200 by vx_device_probe,
+tests/golden/b200_desc.json) and the calibrated per-rung constants (oracle/calib_b200.json,
+the empirical tier of the hybrid analyzer).  Nothing is imported from
+the product package.
+
+Pins: tests/test_oracle_selector.py (SPEC.md worked arithmetic for Eqs. 2-3 and the sieve,
+brute-force argmin, staircase / monotonicity / zero-padding invariants).
+"""
+from __future__ import annotations
+
+import json
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+
+IN_BYTES = {"bf16": 2, "fp16": 2, "fp32": 4}
+OUT_BYTES = {"bf16": 2, "fp16": 2, "fp32": 4}
+
+
+def ceil_div(a: int, b: int) -> int:
+    """ceil(a/b) for a >= 0, b > 0 (R14: every division in the model is a ceiling)."""
+    assert a >= 0 and b > 0
+    return -((-a) // b)
+
+
+# ----------------------------------------------------------------------------------------
+# Eqs. 2-4, literally
+# ----------------------------------------------------------------------------------------
+
+def t_load(nbytes: int, bw_milli: int) -> int:
+    """T_Load / T_Store: "amount of data moved at the current layer divided by the memory
+    bandwidth at that layer".  bw is bytes/cycle scaled by 1000 (R14)."""
+    return ceil_div(nbytes * 1000, bw_milli)
+
+
+def temporal_cost(t_ld: int, trips: int, inner: int, t_st: int) -> int:
+    """Eq. 2: T_Load + (trips-1)*max(T_Load, Cost_{L-1}) + Cost_{L-1} + T_Store."""
+    assert trips >= 1
+    return t_ld + (trips - 1) * max(t_ld, inner) + inner + t_st
+
+
+def parallel_factor(extent: int, units: int) -> int:
+    """Eq. 3: ceil(sizeof(ParallelLoop) / |HardwareUnit|)."""
+    assert extent >= 1 and units >= 1
+    return ceil_div(extent, units)
+
+
+def level_cost(f_parallel: int, t_temporal: int) -> int:
+    """Eq. 4: Cost_L = F_parallel x T_temporal."""
+    return f_parallel * t_temporal
+
+
+# ----------------------------------------------------------------------------------------
+# Alg. 2 building blocks
+# ----------------------------------------------------------------------------------------
+
+def filter_by_isa(cands, is_compatible):
+    """FilterByISA: keep the candidates the base instruction accepts."""
+    return [c for c in cands if is_compatible(c)]
+
+
+def filter_by_multiples(cands, prev_cands, divides):
+    """FilterByMultiples.
+
+    for prev in prevCands: for multiple in GenerateMultiples(prev, cands):
+        filtered.add(multiple); map[multiple].append(prev)
+    GenerateMultiples(prev, cands) = the members of the current layer's candidate range
+    that are integer multiples of prev (R4).  Returns (filtered, map) with
+    filtered in the order of first insertion and map[c] listing prevs in prevCands order.
+    """
+    filtered = []
+    seen = set()
+    cmap = {}
+    for prev in prev_cands:
+        multiples = [c for c in cands if divides(prev, c)]
+        for m in multiples:
+            if m not in seen:
+                seen.add(m)
+                filtered.append(m)
+            cmap.setdefault(m, []).append(prev)
+    return filtered, cmap
+
+
+# ----------------------------------------------------------------------------------------
+# Hardware information (GetHardwareInfo) and calibration data
+# ----------------------------------------------------------------------------------------
+
+def load_descriptor(path: str | None = None) -> dict:
+    path = path or os.path.join(os.path.dirname(_HERE), "tests", "golden", "b200_desc.json")
+    with open(path) as f:
+        return json.load(f)
+
+
+def load_calib(path: str | None = None) -> dict:
+    path = path or os.path.join(_HERE, "calib_b200.json")
+    with open(path) as f:
+        return json.load(f)
+
+
+# ----------------------------------------------------------------------------------------
+# The strategy table ("vx_plan"), sample-free: depends on (K, dtypes, descriptor) only
+# ----------------------------------------------------------------------------------------
+
+UMMA_M_LATTICE = (64, 128, 256)                 # R1
+N_LATTICE = (8, 16, 32, 64, 128, 192, 256)       # R1
+UMMA_K = 16                                      # kind::f16: K = 32 bytes / 2-byte element
+BK_TC = 64                                       # one 128-B swizzle row of 2-byte elements
+SPLITS = (1, 2, 4, 8)                            # R7
+MAX_STAGES = 16                                  # R5
+SMEM_RESERVE = 1024                              # barriers + 1024-B alignment slack
+CLUSTER_MAX = 8                                  # portable cluster size
+
+# kernels that exist in the library (the "implemented" filter, R6):
+#   family 0: tcgen05 cta_group::1, A-tile on the UMMA-M axis   (BM=128; BN in {64,128,256})
+#   family 1: same kernel with A/B swapped (N on UMMA-M, M on UMMA-N; BN in {16,32,64,128})
+#   family 2: fp32 SIMT FFMA (BM, BN, TM, TN) in {(32,32,2,4),(64,64,4,4),(128,64,8,4)}
+IMPL_TC = {(0, 128, 64), (0, 128, 128), (0, 128, 256),
+           (1, 128, 16), (1, 128, 32), (1, 128, 64), (1, 128, 128)}
+SIMT_TILES = ((32, 32, 2, 4), (64, 64, 4, 4), (128, 64, 8, 4))
+SIMT_BK = 16
+FAMILY_NAMES = {0: "umma", 1: "umma_swap", 2: "simt"}
+
+
+def isa_compatible_f16(c) -> bool:
+    """tcgen05.mma.kind::f16 shapes (PTX ISA): M=64 -> N%8==0, 8..256; M=128 -> N%16==0,
+    16..256 (cta_group::1); M=256 -> cta_group::2, N%16==0, 16..256.  K = 16."""
+    um, un, uk = c
+    if uk != UMMA_K:
+        return False
+    if um == 64:
+        return un % 8 == 0 and 8 <= un <= 256
+    if um in (128, 256):
+        return un % 16 == 0 and 16 <= un <= 256
+    return False
+
+
+def build_table(K: int, in_dtype: str, out_dtype: str, desc: dict) -> dict:
+    """Alg. 2 bottom-up over the sm_100a levels; returns {'levels': counts, 'rungs': [...]}.
+
+    L0 instruction tile, L1 TMEM accumulator tile, L2 CTA/SMEM tile, L3 grid schedule.
+    """
+    in_b = IN_BYTES[in_dtype]
+    rungs = []
+    counts = {}
+    if in_dtype in ("bf16", "fp16"):
+        # ---- L0: InitCands (lattice) -> FilterByISA ---------------------------------
+        l0_init = [(um, un, UMMA_K) for um in UMMA_M_LATTICE for un in N_LATTICE]
+        l0 = filter_by_isa(l0_init, isa_compatible_f16)
+        # ---- L1: TMEM accumulator (AM lanes x AN fp32 columns x acc_stages) -----------
+        # InitCands: capacity = TMEM columns (R2: window not applied to TMEM)
+        l1_init = [(am, an, st) for am in UMMA_M_LATTICE for an in N_LATTICE for st in (1, 2)
+                   if st * an <= desc["tmem_cols"]]
+        l1, map1 = filter_by_multiples(
+            l1_init, l0, lambda p, c: c[0] == p[0] and c[1] % p[1] == 0)
+        # ---- L2: CTA tile (BM x BN x BK, S stages) in shared memory ------------------
+        cap = desc["smem_optin"]
+        l2_init = []
+        for (am, an, st) in l1:
+            cg = 2 if am == 256 else 1
+            bm_cta, bn_cta = am // cg, an // cg
+            stage_bytes = (bm_cta + bn_cta) * BK_TC * in_b
+            s_fit = (cap - SMEM_RESERVE) // stage_bytes
+            S = min(MAX_STAGES, s_fit)
+            if S < 2:
+                continue
+            foot = S * stage_bytes + SMEM_RESERVE
+            if foot * 8 < cap:            # utilisation window [1/8, 1] (R3)
+                continue
+            l2_init.append((am, an, BK_TC, S, st))
+        l2, map2 = filter_by_multiples(
+            l2_init, l1,
+            lambda p, c: c[0] % p[0] == 0 and c[1] % p[1] == 0 and c[4] == p[2]
+            and c[2] % UMMA_K == 0)
+        # ---- L3: grid schedule (swap, splits) + implemented filter -------------------
+        kb = ceil_div(K, BK_TC)
+        for (bm, bn, bk, S, st) in l2:
+            cg = 2 if bm == 256 else 1
+            for swap in (0, 1):
+                if (swap, bm, bn) not in IMPL_TC or cg != 1 or st != 2:
+                    continue
+                stage_bytes = (bm + bn) * bk * in_b
+                splits = []
+                for s in SPLITS:
+                    if kb % s != 0 or s * cg > CLUSTER_MAX:
+                        continue
+                    if s > 1 and bm * (bn + 4) * 4 > S * stage_bytes:
+                        continue
+                    splits.append(s)
+                rungs.append({"family": swap, "cg": cg, "um": bm, "un": bn, "acc_stages": st,
+                              "bm": bm, "bn": bn, "bk": bk, "stages": S, "swap": swap,
+                              "splits": splits})
+        counts = {"l0": len(l0), "l1": len(l1), "l2": len(l2), "l3": len(rungs)}
+    elif in_dtype == "fp32":
+        # CUDA-core mode: L0 = FFMA thread tiles, L2 = CTA tiles
+        l0 = [(tm, tn) for (_, _, tm, tn) in SIMT_TILES]
+        l0 = sorted(set(l0))
+        l2_init = []
+        for (bm, bn, tm, tn) in SIMT_TILES:
+            threads = (bm // tm) * (bn // tn)
+            if threads > desc["max_threads_per_block"]:
+                continue
+            l2_init.append((bm, bn, SIMT_BK, tm, tn))
+        l2, _ = filter_by_multiples(l2_init, l0,
+                                    lambda p, c: c[3] == p[0] and c[4] == p[1]
+                                    and c[0] % p[0] == 0 and c[1] % p[1] == 0)
+        for (bm, bn, bk, tm, tn) in l2:
+            rungs.append({"family": 2, "cg": 1, "um": tm, "un": tn, "acc_stages": 1,
+                          "bm": bm, "bn": bn, "bk": bk, "stages": 2, "swap": 0,
+                          "splits": [1]})
+        counts = {"l0": len(l0), "l1": len(l0), "l2": len(l2), "l3": len(rungs)}
+    else:
+        raise ValueError(in_dtype)
+    # deterministic rung ids (R13): lexicographic on (family, bm, bn, stages, swap)
+    rungs.sort(key=lambda r: (r["family"], r["bm"], r["bn"], r["stages"], r["swap"]))
+    for i, r in enumerate(rungs):
+        r["rung_id"] = i
+    return {"K": K, "in": in_dtype, "out": out_dtype, "levels": counts, "rungs": rungs}
+
+
+# ----------------------------------------------------------------------------------------
+# Runtime cost and selection ("vx_plan_select")
+# ----------------------------------------------------------------------------------------
+
+def _calib_for(rung: dict, calib: dict) -> dict:
+    fam = FAMILY_NAMES[rung["family"]]
+    key = "%s_%dx%d" % (fam, rung["bm"], rung["bn"])
+    return calib["rungs"][key]
+
+
+def simt_slots(rung: dict, desc: dict) -> int:
+    bm, bn, bk = rung["bm"], rung["bn"], rung["bk"]
+    threads = (bm // rung["um"]) * (bn // rung["un"])
+    foot = 2 * (bm + bn) * bk * 4 + SMEM_RESERVE
+    occ = min(desc["smem_per_sm"] // foot, desc["max_threads_per_sm"] // threads, 32)
+    return desc["sm_count"] * max(occ, 1)
+
+
+def rung_cost(rung: dict, s: int, batch: int, M: int, N: int, K: int,
+              in_dtype: str, out_dtype: str, desc: dict, calib: dict) -> dict:
+    """Predicted cycles of (rung, split) for the runtime shape."""
+    in_b, out_b = IN_BYTES[in_dtype], OUT_BYTES[out_dtype]
+    cal = _calib_for(rung, calib)
+    hbm = calib["hbm_milli"]
+    bm, bn, bk = rung["bm"], rung["bn"], rung["bk"]
+    # padding only at the outermost (grid) level (Fig. padding)
+    mt, nt = (N, M) if rung["swap"] else (M, N)
+    tm, tn = ceil_div(mt, bm), ceil_div(nt, bn)
+    tiles = batch * tm * tn
+    kb = ceil_div(K, bk)
+    trips = kb // s                                   # sizeof(TemporalLoop) at CTA level (R8)
+    W = tiles * s                                     # sizeof(ParallelLoop) at grid level
+    if rung["family"] == 2:
+        slots = simt_slots(rung, desc)
+    else:
+        slots = desc["max_active_clusters"][str(s * rung["cg"])] * s * rung["cg"]
+    F = parallel_factor(W, slots)                     # Eq. 3 (|HardwareUnit| = slots, R9)
+    active = min(W, slots)
+    if rung["family"] == 2:
+        occ = ceil_div(active, desc["sm_count"])      # CTAs sharing one SM
+        inner = t_load(bm * bn * bk * occ, cal["mac_milli"])
+        l_smem = t_load((bm + bn) * bk * in_b * occ, cal["l2s_milli"])
+    else:
+        inner = t_load(bm * bn * bk, cal["mac_milli"])          # Cost_{L-1}, empirical tier
+        l_smem = t_load((bm + bn) * bk * in_b, cal["l2s_milli"])
+    # HBM share of one k-step: the grid's unique operand bytes leave HBM once, spread over
+    # F waves x trips k-steps that all run at the chip bandwidth (R10)
+    uniq = in_b * batch * K * (mt + nt)
+    l_hbm = t_load(uniq, F * trips * hbm)
+    tl = max(l_smem, l_hbm)                           # T_Load
+    cbytes = out_b * batch * M * N                    # true C bytes (clipped tail rows)
+    st_epi = t_load(bm * bn * out_b, s * cal["epi_milli"])
+    st_hbm = t_load(cbytes, F * hbm)
+    ts = max(st_epi, st_hbm)                          # T_Store
+    if s > 1:
+        ts += t_load((s - 1) * bm * bn * 4, s * calib["dsm_milli"])
+    T = temporal_cost(tl, trips, inner, ts)           # Eq. 2
+    if s == 1 and rung["family"] != 2:
+        # persistent CTA, double-buffered TMEM accumulator (R11): the grid-level PL loop
+        # becomes a temporal loop of F tiles whose "load" is the mainloop and whose
+        # "compute" is the epilogue -> Eq. 2 again at the grid level.
+        tmain = T - ts
+        cost = temporal_cost(tmain, F, ts, 0) + cal["fixed"]
+    else:
+        cost = level_cost(F, T) + cal["fixed"] + (calib["fixed_cluster"] if s > 1 else 0)
+    return {"cost": cost, "tiles_m": tm, "tiles_n": tn, "tiles": tiles, "F": F,
+            "grid": W if s > 1 or rung["family"] == 2 else min(tiles, slots),
+            "padded_work": batch * tm * bm * tn * bn}
+
+
+def select(table: dict, batch: int, M: int, N: int, K: int, desc: dict, calib: dict) -> dict:
+    """Eq. 1 argmin over (rung, split); key (cost, padded_work, rung_id, split) (R13)."""
+    assert M >= 1 and N >= 1 and batch >= 1
+    best = None
+    for r in table["rungs"]:
+        for s in r["splits"]:
+            c = rung_cost(r, s, batch, M, N, K, table["in"], table["out"], desc, calib)
+            key = (c["cost"], c["padded_work"], r["rung_id"], s)
+            if best is None or key < best[0]:
+                best = (key, r, s, c)
+    key, r, s, c = best
+    return {"rung_id": r["rung_id"], "split": s, "tiles_m": c["tiles_m"],
+            "tiles_n": c["tiles_n"], "grid": c["grid"], "cost": c["cost"],
+            "swap": r["swap"], "bm": r["bm"], "bn": r["bn"]}
