@@ -1,0 +1,53 @@
+// vx_calib.cpp -- the empirical tier of Vortex's hybrid analytical-empirical analyzer
+// (Sec. 5.2: "empirical profiling ... on GPUs at both L0 and L1
+// levels. For higher levels, it utilizes an analytical cost model").
+//
+// On sm_100a the L0/L1 behaviour of a rung is summarised by four steady-state rates that
+// are measured ONCE on a B200 (tools/calibrate.py, evidence under profiles/) and compiled
+// in, so vx_plan stays deterministic and sample-free (no shape is ever profiled):
+//   mac_milli  MACs per SM cycle of the rung's MMA issue loop           (Cost_{L-1})
+//   l2s_milli  bytes per SM cycle TMA delivers into this CTA's SMEM ring (T_Load, per CTA)
+//   epi_milli  bytes per SM cycle of the TMEM -> register -> global epilogue (T_Store)
+//   fixed      cycles of prologue (barrier init, TMEM alloc, descriptor fetch) + launch
+// plus chip-wide HBM bandwidth, DSMEM bandwidth and the cluster-launch surcharge.
+// All values are integers scaled x1000 so the selector is exact integer arithmetic (R14).
+//
+// The test side keeps its own copy of these numbers (oracle/calib_b200.json);
+// tests/test_selector_parity.py checks the two agree through vx_plan_dump.
+#include <cstring>
+
+#include "vx_internal.h"
+
+namespace vx {
+
+static const Calib kCalib = {
+    /*hbm_milli=*/3330000,   // 6543 GB/s measured copy bandwidth / 1.965 GHz
+    /*dsm_milli=*/20000,     // ~20 B/cycle DSMEM (B300_MICROARCH.md)
+    /*fixed_cluster=*/1500,  // cluster launch + two cluster barriers
+};
+
+static const RungCalib kRungs[] = {
+    {"umma_128x64", 2730000, 64000, 64000, 3000},
+    {"umma_128x128", 4096000, 64000, 64000, 3000},
+    {"umma_128x256", 4096000, 64000, 64000, 3000},
+    {"umma_swap_128x16", 910000, 64000, 16000, 3000},
+    {"umma_swap_128x32", 1638000, 64000, 16000, 3000},
+    {"umma_swap_128x64", 2730000, 64000, 16000, 3000},
+    {"umma_swap_128x128", 4096000, 64000, 16000, 3000},
+    {"simt_32x32", 128000, 32000, 16000, 2000},
+    {"simt_64x64", 128000, 32000, 16000, 2000},
+    {"simt_128x64", 128000, 32000, 16000, 2000},
+};
+
+const Calib& calib_globals() { return kCalib; }
+
+const RungCalib* calib_lookup(const std::string& key) {
+    for (const auto& r : kRungs)
+        if (key == r.key) return &r;
+    return nullptr;
+}
+
+int calib_count() { return (int)(sizeof(kRungs) / sizeof(kRungs[0])); }
+const RungCalib* calib_at(int i) { return &kRungs[i]; }
+
+}  // namespace vx

@@ -1,0 +1,355 @@
+// vx_dispatch.cu -- runtime half of vx_gemm: validation, CUtensorMap encoding, and the
+// launch of the rung vx_plan_select chose ("compute runtime-specific computational details,
+// such as grid configurations").  Also the device probe (GetHardwareInfo,
+// PAPER.md:1770) and the explicit instantiation table of the ladder kernels.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "vx_internal.h"
+#include "vx_simt.cuh"
+#include "vx_umma.cuh"
+
+namespace vx {
+
+static std::atomic<int64_t> g_launches{0};
+
+// ---- instantiated kernels (the "implemented" filter of the strategy table, R6) -----------
+bool kernel_available(int family, int bm, int bn) {
+    if (family == kUmma) return bm == 128 && (bn == 64 || bn == 128 || bn == 256);
+    if (family == kUmmaSwap) return bm == 128 && (bn == 16 || bn == 32 || bn == 64 || bn == 128);
+    if (family == kSimt) return (bm == 32 && bn == 32) || (bm == 64 && bn == 64) || (bm == 128 && bn == 64);
+    return false;
+}
+
+using UmmaFn = void (*)(const CUtensorMap, const CUtensorMap, const UmmaParams);
+
+template <int BN, bool SWAP>
+static UmmaFn pick_mn(bool b_mn) {
+    // B stored K x N makes B's tile MN-major: it is Q (non-swap) or P (swap)
+    if (SWAP) return b_mn ? (UmmaFn)vx_umma_kernel<BN, true, true, false>
+                          : (UmmaFn)vx_umma_kernel<BN, true, false, false>;
+    return b_mn ? (UmmaFn)vx_umma_kernel<BN, false, false, true>
+                : (UmmaFn)vx_umma_kernel<BN, false, false, false>;
+}
+
+static UmmaFn umma_fn(int family, int bn, bool b_mn) {
+    if (family == kUmma) {
+        switch (bn) {
+        case 64: return pick_mn<64, false>(b_mn);
+        case 128: return pick_mn<128, false>(b_mn);
+        case 256: return pick_mn<256, false>(b_mn);
+        }
+    } else if (family == kUmmaSwap) {
+        switch (bn) {
+        case 16: return pick_mn<16, true>(b_mn);
+        case 32: return pick_mn<32, true>(b_mn);
+        case 64: return pick_mn<64, true>(b_mn);
+        case 128: return pick_mn<128, true>(b_mn);
+        }
+    }
+    return nullptr;
+}
+
+using SimtFn = void (*)(const float*, const float*, float*, int, int, int, int, long long,
+                        long long, long long, int, int);
+
+static SimtFn simt_fn(int bm, int bn, int* threads) {
+    if (bm == 32 && bn == 32) { *threads = 128; return vx_simt_kernel<32, 32, 2, 4>; }
+    if (bm == 64 && bn == 64) { *threads = 256; return vx_simt_kernel<64, 64, 4, 4>; }
+    if (bm == 128 && bn == 64) { *threads = 256; return vx_simt_kernel<128, 64, 8, 4>; }
+    return nullptr;
+}
+
+static int64_t umma_smem_bytes(int bn, int stages) {
+    return (int64_t)stages * (128 + bn) * kBkTc * 2 + kSmemReserve;
+}
+
+static vx_status cuda_fail(cudaError_t e, const char* what) {
+    set_error("%s: %s", what, cudaGetErrorString(e));
+    return VX_ERR_CUDA;
+}
+
+// one-time per-kernel attribute setup (max dynamic smem; cluster dims are per launch)
+static std::mutex g_attr_mu;
+static vx_status ensure_attr(const void* fn, int64_t smem) {
+    static const void* done[64];
+    static int64_t done_smem[64];
+    static int ndone = 0;
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    for (int i = 0; i < ndone; ++i)
+        if (done[i] == fn && done_smem[i] >= smem) return VX_OK;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+    for (int i = 0; i < ndone; ++i)
+        if (done[i] == fn) { done_smem[i] = smem; return VX_OK; }
+    if (ndone < 64) { done[ndone] = fn; done_smem[ndone] = smem; ++ndone; }
+    return VX_OK;
+}
+
+// ---- CUtensorMap encoding via the driver entry point (no -lcuda link dependency) -------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess && q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    return fn;
+}
+
+// 3-D map over a 16-bit matrix stored [batch][rows][inner] (inner contiguous):
+// dims {inner, rows, batch}; box {64, box_rows, 1}; 128-B swizzle; OOB -> zeros.
+static vx_status make_map(CUtensorMap* map, const void* base, vx_dtype dt, int64_t inner,
+                          int64_t rows, int64_t batch, int64_t ld, int64_t bstride,
+                          int box_inner, int box_rows) {
+    EncodeTiledFn enc = encode_fn();
+    if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return VX_ERR_CUDA; }
+    cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)rows, (cuuint64_t)batch};
+    cuuint64_t strides[2] = {(cuuint64_t)ld * 2, (cuuint64_t)bstride * 2};
+    cuuint32_t box[3] = {(cuuint32_t)box_inner, (cuuint32_t)box_rows, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(map, dt == VX_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                     3, const_cast<void*>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        set_error("cuTensorMapEncodeTiled failed (%d): inner=%lld rows=%lld batch=%lld ld=%lld",
+                  (int)r, (long long)inner, (long long)rows, (long long)batch, (long long)ld);
+        return VX_ERR_CUDA;
+    }
+    return VX_OK;
+}
+
+static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+vx_status launch(const vx_plan_s* p, const vx_choice& ch, int64_t batch, int64_t M, int64_t N,
+                 int64_t K, const void* A, int64_t sA, const void* B, int64_t sB, void* C,
+                 int64_t sC, void* stream) {
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const vx::Rung& r = p->rungs[ch.rung_id];
+    if (r.family == kSimt) {
+        int threads = 0;
+        SimtFn fn = simt_fn(r.bm, r.bn, &threads);
+        if (!fn) { set_error("no SIMT kernel %dx%d", r.bm, r.bn); return VX_ERR_UNSUPPORTED; }
+        const int tm = (int)cdiv(M, r.bm), tn = (int)cdiv(N, r.bn);
+        const int64_t grid = batch * (int64_t)tm * tn;
+        fn<<<(unsigned)grid, threads, 0, st>>>((const float*)A, (const float*)B, (float*)C, (int)M,
+                                               (int)N, (int)K, p->bl == VX_B_NK, sA, sB, sC, tm, tn);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_fail(e, "SIMT launch");
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        return VX_OK;
+    }
+    const bool swap = r.swap != 0;
+    const bool b_mn = p->bl == VX_B_KN;
+    UmmaFn fn = umma_fn(r.family, r.bn, b_mn);
+    if (!fn) { set_error("no tcgen05 kernel for rung %d", r.rung_id); return VX_ERR_UNSUPPORTED; }
+    const int64_t smem = umma_smem_bytes(r.bn, r.stages);
+    vx_status s = ensure_attr((const void*)fn, smem);
+    if (s != VX_OK) return s;
+
+    // tensor maps: A [batch][M][K] K-major; B [batch][N][K] (NK) or [batch][K][N] (KN)
+    CUtensorMap mapA, mapB;
+    const int a_box = swap ? r.bn : 128;  // A is P (box 128 rows) or Q (box BN rows)
+    s = make_map(&mapA, A, p->in, K, M, batch, K, batch > 1 ? sA : M * K, 64, a_box);
+    if (s != VX_OK) return s;
+    if (b_mn) {
+        s = make_map(&mapB, B, p->in, N, K, batch, N, batch > 1 ? sB : K * N, 64, 64);
+    } else {
+        const int b_box = swap ? 128 : r.bn;
+        s = make_map(&mapB, B, p->in, K, N, batch, K, batch > 1 ? sB : N * K, 64, b_box);
+    }
+    if (s != VX_OK) return s;
+
+    UmmaParams prm;
+    prm.M = (int)M;
+    prm.N = (int)N;
+    prm.tiles_p = ch.tiles_m;
+    prm.tiles_q = ch.tiles_n;
+    prm.num_tiles = (int)(batch * (int64_t)ch.tiles_m * ch.tiles_n);
+    prm.kb_total = (int)cdiv(K, kBkTc);
+    prm.splits = ch.split;
+    prm.stages = r.stages;
+    prm.out_kind = p->out == VX_BF16 ? 0 : p->out == VX_FP16 ? 1 : 2;
+    const uint32_t fmt = p->in == VX_BF16 ? 1u : 0u;
+    const uint32_t p_major = (swap && b_mn) ? 1u : 0u;   // P operand MN-major?
+    const uint32_t q_major = (!swap && b_mn) ? 1u : 0u;  // Q operand MN-major?
+    prm.idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (p_major << 15) | (q_major << 16) |
+                ((uint32_t)(r.bn >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    prm.C = C;
+    prm.ldc = N;
+    prm.sC = batch > 1 ? sC : M * N;
+
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)ch.grid, 1, 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = (size_t)smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    if (ch.split > 1) {
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = (unsigned)ch.split;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+    }
+    // P operand (UMMA-M axis) first: A for family 0, B for the swapped family
+    const CUtensorMap& mapP = swap ? mapB : mapA;
+    const CUtensorMap& mapQ = swap ? mapA : mapB;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, fn, mapP, mapQ, prm);
+    if (e != cudaSuccess) return cuda_fail(e, "tcgen05 launch");
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return VX_OK;
+}
+
+vx_status prepare_kernels(const vx_plan_s* p) {
+    for (const vx::Rung& r : p->rungs) {
+        if (r.family == kSimt) continue;
+        UmmaFn fn = umma_fn(r.family, r.bn, p->bl == VX_B_KN);
+        if (!fn) continue;
+        vx_status s = ensure_attr((const void*)fn, umma_smem_bytes(r.bn, r.stages));
+        if (s != VX_OK) return s;
+    }
+    return VX_OK;
+}
+
+}  // namespace vx
+
+using namespace vx;
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+static vx_status check_args(const vx_plan_s* p, int64_t batch, int64_t M, int64_t N, int64_t K,
+                            const void* A, int64_t sA, const void* B, int64_t sB, const void* C,
+                            int64_t sC) {
+    if (!p) { set_error("NULL plan"); return VX_ERR_INVALID; }
+    if (batch < 1 || M < 0 || N < 1 || K < 1) { set_error("bad sizes"); return VX_ERR_INVALID; }
+    if (K != p->K) { set_error("K=%lld does not match the plan's K=%lld", (long long)K, (long long)p->K); return VX_ERR_INVALID; }
+    if (p->N > 0 && N != p->N) { set_error("N=%lld does not match the plan's N=%lld", (long long)N, (long long)p->N); return VX_ERR_INVALID; }
+    if (!A || !B || !C) { set_error("NULL operand"); return VX_ERR_INVALID; }
+    if (batch > 1 && (sA < M * K || sB < N * K || sC < M * N)) { set_error("batch strides overlap"); return VX_ERR_INVALID; }
+    if (M > 0x7fffffffLL || N > 0x7fffffffLL) { set_error("M, N must fit in int32"); return VX_ERR_INVALID; }
+    if (p->in != VX_FP32) {
+        if (N % 8 || K % 8) { set_error("16-bit inputs need N %% 8 == 0 and K %% 8 == 0"); return VX_ERR_ALIGN; }
+        if (!aligned16(A) || !aligned16(B) || !aligned16(C)) { set_error("operands must be 16-byte aligned"); return VX_ERR_ALIGN; }
+        if (batch > 1 && (sA % 8 || sB % 8 || sC % 8)) { set_error("batch strides must be multiples of 8 elements"); return VX_ERR_ALIGN; }
+    }
+    return VX_OK;
+}
+
+extern "C" {
+
+vx_status vx_device_probe(int device, vx_device_desc* out) {
+    if (!out) { set_error("NULL argument"); return VX_ERR_INVALID; }
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n) {
+        cudaGetLastError();
+        set_error("CUDA device %d not available", device);
+        return VX_ERR_NODEV;
+    }
+    cudaDeviceProp pr;
+    cudaError_t e = cudaGetDeviceProperties(&pr, device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceProperties");
+    if (pr.major != 10) { set_error("device %d is sm_%d%d, need sm_100", device, pr.major, pr.minor); return VX_ERR_NODEV; }
+    memset(out, 0, sizeof(*out));
+    out->sm_count = pr.multiProcessorCount;
+    out->smem_optin = (int32_t)pr.sharedMemPerBlockOptin;
+    out->smem_per_sm = (int32_t)pr.sharedMemPerMultiprocessor;
+    out->max_threads_per_block = pr.maxThreadsPerBlock;
+    out->max_threads_per_sm = pr.maxThreadsPerMultiProcessor;
+    out->tmem_cols = 512;
+    out->cc_major = pr.major;
+    out->cc_minor = pr.minor;
+    int clk = 0;
+    cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, device);
+    out->clock_khz = clk;
+    out->l2_bytes = pr.l2CacheSize;
+    // resident clusters of 1/2/4/8 full-SMEM CTAs of the ladder kernel
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(device);
+    UmmaFn fn = umma_fn(kUmma, 128, false);
+    const int64_t smem = (int64_t)out->smem_optin;
+    vx_status s = ensure_attr((const void*)fn, smem);
+    if (s != VX_OK) { cudaSetDevice(cur); return s; }
+    const int sizes[4] = {1, 2, 4, 8};
+    for (int i = 0; i < 4; ++i) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(sizes[i] * 64, 1, 1);
+        cfg.blockDim = dim3(kThreads, 1, 1);
+        cfg.dynamicSmemBytes = (size_t)smem;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = sizes[i];
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int nc = 0;
+        e = cudaOccupancyMaxActiveClusters(&nc, fn, &cfg);
+        if (e != cudaSuccess) { cudaSetDevice(cur); return cuda_fail(e, "cudaOccupancyMaxActiveClusters"); }
+        out->max_active_clusters[i] = nc;
+    }
+    cudaSetDevice(cur);
+    return VX_OK;
+}
+
+vx_status vx_gemm_ex(vx_plan_t p, int64_t batch, int64_t M, int64_t N, int64_t K, const void* A,
+                     int64_t sA, const void* B, int64_t sB, void* C, int64_t sC,
+                     int32_t force_rung, int32_t force_split, void* stream, vx_choice* used) {
+    vx_status s = check_args(p, batch, M, N, K, A, sA, B, sB, C, sC);
+    if (s != VX_OK) return s;
+    if (M == 0) return VX_OK;
+    vx_choice ch;
+    s = select_choice(p, batch, M, N, force_rung, force_split, &ch);
+    if (s != VX_OK) return s;
+    if (used) *used = ch;
+    return launch(p, ch, batch, M, N, K, A, sA, B, sB, C, sC, stream);
+}
+
+vx_status vx_gemm_batched(vx_plan_t p, int64_t batch, int64_t M, int64_t N, int64_t K,
+                          const void* A, int64_t sA, const void* B, int64_t sB, void* C,
+                          int64_t sC, void* stream) {
+    return vx_gemm_ex(p, batch, M, N, K, A, sA, B, sB, C, sC, -1, 0, stream, nullptr);
+}
+
+vx_status vx_gemm(vx_plan_t p, int64_t M, int64_t N, int64_t K, const void* A, const void* B,
+                  void* C, void* stream) {
+    return vx_gemm_ex(p, 1, M, N, K, A, M * K, B, N * K, C, M * N, -1, 0, stream, nullptr);
+}
+
+vx_status vx_gemm_host(vx_plan_t p, int64_t batch, int64_t M, int64_t N, int64_t K,
+                       const void* A, const void* B, void* C, void* dA, void* dB, void* dC,
+                       void* stream) {
+    if (!p || !A || !B || !C || !dA || !dB || !dC) { set_error("NULL argument"); return VX_ERR_INVALID; }
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const int ib = in_bytes(p->in), ob = out_bytes(p->out);
+    const size_t a_bytes = (size_t)(batch * M * K) * ib, b_bytes = (size_t)(batch * N * K) * ib;
+    const size_t c_bytes = (size_t)(batch * M * N) * ob;
+    cudaError_t e = cudaMemcpyAsync(dA, A, a_bytes, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dB, B, b_bytes, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
+    vx_status s = vx_gemm_ex(p, batch, M, N, K, dA, M * K, dB, N * K, dC, M * N, -1, 0, stream, nullptr);
+    if (s != VX_OK) return s;
+    e = cudaMemcpyAsync(C, dC, c_bytes, cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) return cuda_fail(e, "D2H copy");
+    return VX_OK;
+}
+
+int64_t vx_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+}  // extern "C"

@@ -1,0 +1,88 @@
+// vx_internal.h -- host-side internals shared by vx_plan.cpp (strategy table, cost model,
+// selection) and vx_dispatch.cu (tensor maps, launches).  Product code only.
+#pragma once
+
+#include <atomic>
+#include <memory>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "vx.h"
+
+namespace vx {
+
+// Kernel families of the ladder's top level
+enum Family : int32_t { kUmma = 0, kUmmaSwap = 1, kSimt = 2 };
+
+constexpr int kBkTc = 64;          // one 128-B swizzle row of 2-byte elements
+constexpr int kUmmaK = 16;         // kind::f16 instruction K
+constexpr int kMaxStages = 16;     // R5
+constexpr int kSmemReserve = 2048; // barriers + 1024-B alignment slack
+constexpr int kClusterMax = 8;     // portable cluster size
+constexpr int kSimtBk = 16;
+
+// One rung = one full chain L0 -> L1 -> L2 -> L3 of the strategy table (Alg. 2 map).
+struct Rung {
+    int32_t rung_id;
+    int32_t family;
+    int32_t cg;          // cta_group (1 or 2)
+    int32_t um, un;      // L0: instruction tile (tcgen05 M x N) or FFMA thread tile
+    int32_t acc_stages;  // L1: TMEM accumulator buffers
+    int32_t bm, bn, bk;  // L2: CTA tile
+    int32_t stages;      // L2: SMEM pipeline depth
+    int32_t swap;        // L3: operand swap
+    std::vector<int32_t> splits;  // L3: admissible K-loop splits
+    // calibration (empirical tier), scaled x1000
+    int64_t mac_milli, l2s_milli, epi_milli, fixed;
+};
+
+struct Calib {
+    int64_t hbm_milli, dsm_milli, fixed_cluster;
+};
+
+struct RungCalib {
+    const char* key;
+    int64_t mac_milli, l2s_milli, epi_milli, fixed;
+};
+
+// compiled-in calibration table (vx_calib.cpp)
+const Calib& calib_globals();
+const RungCalib* calib_lookup(const std::string& key);
+int calib_count();
+const RungCalib* calib_at(int i);
+
+struct LevelCounts {
+    int64_t l0, l1, l2, l3;
+};
+
+}  // namespace vx
+
+struct vx_plan_s {
+    int64_t N;  // 0 = dynamic
+    int64_t K;
+    vx_dtype in, out;
+    vx_blayout bl;
+    vx_device_desc desc;
+    int device;  // -1 when built from an explicit descriptor
+    std::vector<vx::Rung> rungs;
+    vx::LevelCounts counts;
+    // memo of selections for batch == 1, static N, M in [1, kMemo]
+    static constexpr int64_t kMemo = 16384;
+    std::vector<vx_choice> memo;
+    std::unique_ptr<std::atomic<uint8_t>[]> memo_state;
+};
+
+namespace vx {
+// vx_plan.cpp
+vx_status select_choice(const vx_plan_s* p, int64_t batch, int64_t M, int64_t N,
+                        int32_t force_rung, int32_t force_split, vx_choice* out);
+int in_bytes(vx_dtype d);
+int out_bytes(vx_dtype d);
+void set_error(const char* fmt, ...);
+// vx_dispatch.cu
+vx_status launch(const vx_plan_s* p, const vx_choice& ch, int64_t batch, int64_t M, int64_t N,
+                 int64_t K, const void* A, int64_t sA, const void* B, int64_t sB, void* C,
+                 int64_t sC, void* stream);
+vx_status prepare_kernels(const vx_plan_s* p);
+}  // namespace vx

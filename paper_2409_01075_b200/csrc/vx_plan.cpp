@@ -1,0 +1,426 @@
+// vx_plan.cpp -- the offline strategy table and the runtime analytical selector of Vortex
+// (arXiv 2409.01075) for sm_100a.  Host-only C++, no CUDA calls: a plan built with
+// vx_plan_ex and a captured descriptor can be planned and selected on a CPU-only host.
+//
+//   vx_plan         Alg. 2 "Candidates Generation Algorithm":
+//                   L0 InitCands -> FilterByISA; L>=1 InitCands -> FilterByMultiples + map,
+//                   over the sm_100a hierarchy of DESIGN.md 3.1:
+//                     L0 tcgen05.mma.kind::f16 instruction tile (UM x UN x 16)
+//                     L1 TMEM accumulator (UM lanes x AN fp32 columns x acc_stages)
+//                     L2 CTA tile in SMEM (BM x BN x 64, S-stage TMA ring)
+//                     L3 grid schedule (operand swap, K-split s over a CTA cluster)
+//   vx_plan_select  Eqs. 2-4 evaluated per (rung, split) for the
+//                   runtime shape in integer cycles, argmin Eq. 1,
+//                   grid configuration.  DESIGN.md 3.3 is the spec; the
+//                   readings R1-R14 it lists are cited inline.
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <set>
+#include <string>
+#include <tuple>
+
+#include "vx_internal.h"
+
+namespace vx {
+
+bool kernel_available(int family, int bm, int bn);  // vx_dispatch.cu
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+int in_bytes(vx_dtype d) { return d == VX_FP32 ? 4 : 2; }
+int out_bytes(vx_dtype d) { return d == VX_FP32 ? 4 : 2; }
+
+static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// ---- Eqs. 2-4 --------------------------------------------------------------------------
+// T_Load / T_Store = bytes moved / bandwidth of that layer, ceiling (R14)
+static inline int64_t t_move(int64_t bytes, int64_t bw_milli) { return cdiv(bytes * 1000, bw_milli); }
+// Eq. 2: T_Load + (trips-1) max(T_Load, Cost_{L-1}) + Cost_{L-1} + T_Store
+static inline int64_t eq2(int64_t tl, int64_t trips, int64_t inner, int64_t ts) {
+    return tl + (trips - 1) * std::max(tl, inner) + inner + ts;
+}
+// Eq. 3: ceil(sizeof(ParallelLoop) / |HardwareUnit|)
+static inline int64_t eq3(int64_t extent, int64_t units) { return cdiv(extent, units); }
+
+// ---- Alg. 2 over the sm_100a levels -----------------------------------------------------
+namespace {
+
+struct L0 { int um, un, uk; };
+struct L1 { int am, an, st; };
+struct L2 { int bm, bn, bk, S, st; };
+
+const int kUmLattice[] = {64, 128, 256};                  // R1
+const int kNLattice[] = {8, 16, 32, 64, 128, 192, 256};   // R1
+
+// tcgen05.mma.kind::f16 legality (PTX ISA shape table)
+bool isa_ok(const L0& c) {
+    if (c.uk != kUmmaK) return false;
+    if (c.um == 64) return c.un % 8 == 0 && c.un >= 8 && c.un <= 256;
+    if (c.um == 128 || c.um == 256) return c.un % 16 == 0 && c.un >= 16 && c.un <= 256;
+    return false;
+}
+
+// FilterByMultiples: for prev in prevCands, for each candidate that is an integer multiple
+// of prev: keep it (first-insertion order) and record the link.
+template <class C, class P, class Div>
+std::vector<C> sieve(const std::vector<C>& cands, const std::vector<P>& prev, Div divides,
+                     int64_t* links) {
+    std::vector<C> out;
+    std::vector<char> taken(cands.size(), 0);
+    int64_t nl = 0;
+    for (const P& p : prev)
+        for (size_t i = 0; i < cands.size(); ++i)
+            if (divides(p, cands[i])) {
+                ++nl;
+                if (!taken[i]) { taken[i] = 1; out.push_back(cands[i]); }
+            }
+    if (links) *links = nl;
+    return out;
+}
+
+const char* family_name(int f) { return f == kUmma ? "umma" : f == kUmmaSwap ? "umma_swap" : "simt"; }
+
+}  // namespace
+
+static vx_status build_rungs(vx_plan_s* p) {
+    const vx_device_desc& d = p->desc;
+    std::vector<Rung> rungs;
+    if (p->in == VX_BF16 || p->in == VX_FP16) {
+        const int in_b = 2;
+        // L0: InitCands = lattice; FilterByISA
+        std::vector<L0> l0;
+        for (int um : kUmLattice)
+            for (int un : kNLattice) {
+                L0 c{um, un, kUmmaK};
+                if (isa_ok(c)) l0.push_back(c);
+            }
+        // L1: TMEM accumulators within the column capacity (R2: no window on TMEM)
+        std::vector<L1> l1i;
+        for (int am : kUmLattice)
+            for (int an : kNLattice)
+                for (int st = 1; st <= 2; ++st)
+                    if (st * an <= d.tmem_cols) l1i.push_back({am, an, st});
+        std::vector<L1> l1 = sieve(l1i, l0, [](const L0& a, const L1& c) {
+            return c.am == a.um && c.an % a.un == 0; }, nullptr);
+        // L2: CTA tiles; stage count = deepest ring that fits SMEM; window [1/8, 1] (R3, R5)
+        std::vector<L2> l2i;
+        for (const L1& a : l1) {
+            int cg = a.am == 256 ? 2 : 1;
+            int64_t stage = (int64_t)(a.am / cg + a.an / cg) * kBkTc * in_b;
+            int64_t fit = (d.smem_optin - kSmemReserve) / stage;
+            int S = (int)std::min<int64_t>(kMaxStages, fit);
+            if (S < 2) continue;
+            int64_t foot = S * stage + kSmemReserve;
+            if (foot * 8 < d.smem_optin) continue;
+            l2i.push_back({a.am, a.an, kBkTc, S, a.st});
+        }
+        std::vector<L2> l2 = sieve(l2i, l1, [](const L1& a, const L2& c) {
+            return c.bm % a.am == 0 && c.bn % a.an == 0 && c.st == a.st && c.bk % kUmmaK == 0; },
+            nullptr);
+        // L3: grid schedules over implemented kernels (R6), splits dividing the k-blocks (R7)
+        const int64_t kb = cdiv(p->K, kBkTc);
+        for (const L2& c : l2) {
+            int cg = c.bm == 256 ? 2 : 1;
+            for (int swap = 0; swap <= 1; ++swap) {
+                int fam = swap ? kUmmaSwap : kUmma;
+                if (cg != 1 || c.st != 2 || !kernel_available(fam, c.bm, c.bn)) continue;
+                int64_t stage = (int64_t)(c.bm + c.bn) * c.bk * in_b;
+                Rung r{};
+                r.family = fam; r.cg = cg; r.um = c.bm; r.un = c.bn; r.acc_stages = c.st;
+                r.bm = c.bm; r.bn = c.bn; r.bk = c.bk; r.stages = c.S; r.swap = swap;
+                for (int s : {1, 2, 4, 8}) {
+                    if (kb % s != 0 || s * cg > kClusterMax) continue;
+                    if (s > 1 && (int64_t)c.bm * (c.bn + 4) * 4 > c.S * stage) continue;
+                    r.splits.push_back(s);
+                }
+                rungs.push_back(r);
+            }
+        }
+        p->counts = {(int64_t)l0.size(), (int64_t)l1.size(), (int64_t)l2.size(), (int64_t)rungs.size()};
+    } else {
+        // CUDA-core mode: L0 FFMA thread tiles, L2 CTA tiles (BK = 16)
+        struct T { int bm, bn, tm, tn; };
+        const T tiles[] = {{32, 32, 2, 4}, {64, 64, 4, 4}, {128, 64, 8, 4}};
+        std::set<std::pair<int, int>> l0;
+        for (const T& t : tiles) l0.insert({t.tm, t.tn});
+        int64_t n2 = 0;
+        for (const T& t : tiles) {
+            int threads = (t.bm / t.tm) * (t.bn / t.tn);
+            if (threads > d.max_threads_per_block) continue;
+            if (t.bm % t.tm || t.bn % t.tn) continue;
+            ++n2;
+            if (!kernel_available(kSimt, t.bm, t.bn)) continue;
+            Rung r{};
+            r.family = kSimt; r.cg = 1; r.um = t.tm; r.un = t.tn; r.acc_stages = 1;
+            r.bm = t.bm; r.bn = t.bn; r.bk = kSimtBk; r.stages = 2; r.swap = 0;
+            r.splits = {1};
+            rungs.push_back(r);
+        }
+        p->counts = {(int64_t)l0.size(), (int64_t)l0.size(), n2, (int64_t)rungs.size()};
+    }
+    // deterministic ids (R13)
+    std::sort(rungs.begin(), rungs.end(), [](const Rung& a, const Rung& b) {
+        return std::tie(a.family, a.bm, a.bn, a.stages, a.swap) <
+               std::tie(b.family, b.bm, b.bn, b.stages, b.swap); });
+    for (size_t i = 0; i < rungs.size(); ++i) {
+        Rung& r = rungs[i];
+        r.rung_id = (int32_t)i;
+        char key[64];
+        snprintf(key, sizeof key, "%s_%dx%d", family_name(r.family), r.bm, r.bn);
+        const RungCalib* c = calib_lookup(key);
+        if (!c) { set_error("no calibration for rung %s", key); return VX_ERR_UNSUPPORTED; }
+        r.mac_milli = c->mac_milli; r.l2s_milli = c->l2s_milli;
+        r.epi_milli = c->epi_milli; r.fixed = c->fixed;
+    }
+    if (rungs.empty()) { set_error("strategy table is empty"); return VX_ERR_UNSUPPORTED; }
+    p->rungs = std::move(rungs);
+    return VX_OK;
+}
+
+// ---- runtime cost ----------------------------------------------------------
+static void rung_cost(const vx_plan_s* p, const Rung& r, int s, int64_t batch, int64_t M,
+                      int64_t N, vx_choice* o) {
+    const vx_device_desc& d = p->desc;
+    const Calib& cal = calib_globals();
+    const int64_t K = p->K;
+    const int in_b = in_bytes(p->in), out_b = out_bytes(p->out);
+    const int64_t bm = r.bm, bn = r.bn, bk = r.bk;
+    // padding only at the outermost level (fig:padding)
+    const int64_t mt = r.swap ? N : M, nt = r.swap ? M : N;
+    const int64_t tm = cdiv(mt, bm), tn = cdiv(nt, bn);
+    const int64_t tiles = batch * tm * tn;
+    const int64_t kb = cdiv(K, bk);
+    const int64_t trips = kb / s;            // sizeof(TemporalLoop) at the CTA level (R8)
+    const int64_t W = tiles * s;             // sizeof(ParallelLoop) at the grid level
+    int64_t slots;
+    if (r.family == kSimt) {
+        int64_t threads = (bm / r.um) * (bn / r.un);
+        int64_t foot = 2 * (bm + bn) * bk * 4 + kSmemReserve;
+        int64_t occ = std::min<int64_t>(std::min<int64_t>(d.smem_per_sm / foot,
+                                        d.max_threads_per_sm / threads), 32);
+        slots = (int64_t)d.sm_count * std::max<int64_t>(occ, 1);
+    } else {
+        int ci = s * r.cg == 1 ? 0 : s * r.cg == 2 ? 1 : s * r.cg == 4 ? 2 : 3;
+        slots = (int64_t)d.max_active_clusters[ci] * s * r.cg;
+    }
+    const int64_t F = eq3(W, slots);         // Eq. 3, |HardwareUnit| = resident CTAs (R9)
+    const int64_t active = std::min(W, slots);
+    int64_t inner, l_smem;
+    if (r.family == kSimt) {
+        int64_t occ = cdiv(active, d.sm_count);
+        inner = t_move(bm * bn * bk * occ, r.mac_milli);
+        l_smem = t_move((bm + bn) * bk * in_b * occ, r.l2s_milli);
+    } else {
+        inner = t_move(bm * bn * bk, r.mac_milli);           // Cost_{L-1}
+        l_smem = t_move((bm + bn) * bk * in_b, r.l2s_milli);
+    }
+    const int64_t uniq = (int64_t)in_b * batch * K * (mt + nt);
+    const int64_t l_hbm = t_move(uniq, F * trips * cal.hbm_milli);   // R10
+    const int64_t tl = std::max(l_smem, l_hbm);                       // T_Load
+    const int64_t cbytes = (int64_t)out_b * batch * M * N;
+    int64_t ts = std::max(t_move(bm * bn * out_b, s * r.epi_milli), t_move(cbytes, F * cal.hbm_milli));
+    if (s > 1) ts += t_move((int64_t)(s - 1) * bm * bn * 4, s * cal.dsm_milli);
+    const int64_t T = eq2(tl, trips, inner, ts);                      // Eq. 2
+    int64_t cost;
+    if (s == 1 && r.family != kSimt) {
+        // persistent CTA + double-buffered TMEM (R11): Eq. 2 at the grid level
+        cost = eq2(T - ts, F, ts, 0) + r.fixed;
+    } else {
+        cost = F * T + r.fixed + (s > 1 ? cal.fixed_cluster : 0);    // Eq. 4
+    }
+    o->rung_id = r.rung_id;
+    o->split = s;
+    o->family = r.family;
+    o->swap = r.swap;
+    o->bm = r.bm;
+    o->bn = r.bn;
+    o->stages = r.stages;
+    o->tiles_m = (int32_t)tm;
+    o->tiles_n = (int32_t)tn;
+    o->grid = (int32_t)((s > 1 || r.family == kSimt) ? W : std::min(tiles, slots));
+    o->cluster = s;
+    o->reserved = 0;
+    o->cost = cost;
+}
+
+static inline int64_t padded_work(const vx_choice& c, int64_t batch) {
+    return batch * (int64_t)c.tiles_m * c.bm * (int64_t)c.tiles_n * c.bn;
+}
+
+vx_status select_choice(const vx_plan_s* p, int64_t batch, int64_t M, int64_t N,
+                        int32_t force_rung, int32_t force_split, vx_choice* out) {
+    if (!p || !out) { set_error("NULL argument"); return VX_ERR_INVALID; }
+    if (batch < 1 || M < 1 || N < 1) { set_error("batch, M, N must be >= 1"); return VX_ERR_INVALID; }
+    if (p->N > 0 && N != p->N) { set_error("N=%lld does not match the plan's N=%lld", (long long)N, (long long)p->N); return VX_ERR_INVALID; }
+    if (force_rung >= 0) {
+        if (force_rung >= (int32_t)p->rungs.size()) { set_error("rung %d not in table", force_rung); return VX_ERR_INVALID; }
+        const Rung& r = p->rungs[force_rung];
+        if (std::find(r.splits.begin(), r.splits.end(), force_split) == r.splits.end()) {
+            set_error("split %d not admissible for rung %d", force_split, force_rung);
+            return VX_ERR_INVALID;
+        }
+        rung_cost(p, r, force_split, batch, M, N, out);
+        return VX_OK;
+    }
+    const bool memo = batch == 1 && p->N > 0 && M <= vx_plan_s::kMemo;
+    if (memo && p->memo_state[M].load(std::memory_order_acquire) == 2) {
+        *out = p->memo[M];
+        return VX_OK;
+    }
+    // Eq. 1 argmin, key (cost, padded work, rung_id, split) -- a total order (R13)
+    bool have = false;
+    vx_choice best{};
+    for (const Rung& r : p->rungs)
+        for (int s : r.splits) {
+            vx_choice c;
+            rung_cost(p, r, s, batch, M, N, &c);
+            if (!have || std::make_tuple(c.cost, padded_work(c, batch), c.rung_id, c.split) <
+                             std::make_tuple(best.cost, padded_work(best, batch), best.rung_id, best.split)) {
+                best = c;
+                have = true;
+            }
+        }
+    *out = best;
+    if (memo) {
+        uint8_t expect = 0;
+        if (p->memo_state[M].compare_exchange_strong(expect, 1, std::memory_order_acq_rel)) {
+            const_cast<vx_plan_s*>(p)->memo[M] = best;
+            p->memo_state[M].store(2, std::memory_order_release);
+        }
+    }
+    return VX_OK;
+}
+
+}  // namespace vx
+
+using namespace vx;
+
+static const char* dt_name(vx_dtype d) { return d == VX_BF16 ? "bf16" : d == VX_FP16 ? "fp16" : "fp32"; }
+
+extern "C" {
+
+int32_t vx_abi_version(void) { return VX_ABI_VERSION; }
+
+const char* vx_status_str(vx_status s) {
+    switch (s) {
+    case VX_OK: return "VX_OK";
+    case VX_ERR_INVALID: return "VX_ERR_INVALID";
+    case VX_ERR_UNSUPPORTED: return "VX_ERR_UNSUPPORTED";
+    case VX_ERR_ALIGN: return "VX_ERR_ALIGN";
+    case VX_ERR_CUDA: return "VX_ERR_CUDA";
+    case VX_ERR_NODEV: return "VX_ERR_NODEV";
+    case VX_ERR_OOM: return "VX_ERR_OOM";
+    case VX_ERR_BUFFER: return "VX_ERR_BUFFER";
+    }
+    return "VX_ERR_UNKNOWN";
+}
+
+const char* vx_last_error(void) { return g_err; }
+
+vx_status vx_plan_ex(int64_t N, int64_t K, vx_dtype in, vx_dtype out, vx_blayout bl,
+                     const vx_device_desc* desc, vx_plan_t* plan) {
+    g_err[0] = 0;
+    if (!desc || !plan) { set_error("NULL argument"); return VX_ERR_INVALID; }
+    *plan = nullptr;
+    if (N < 0 || K <= 0) { set_error("need N >= 0 (0 = dynamic) and K > 0"); return VX_ERR_INVALID; }
+    if ((int)in < 0 || (int)in > 2 || (int)out < 0 || (int)out > 2 || ((int)bl != 0 && (int)bl != 1)) {
+        set_error("bad dtype or layout enum"); return VX_ERR_INVALID;
+    }
+    if (in == VX_FP32 && out != VX_FP32) { set_error("fp32 inputs need fp32 output"); return VX_ERR_UNSUPPORTED; }
+    if (in != VX_FP32 && (K % 8 != 0 || (N > 0 && N % 8 != 0))) {
+        set_error("16-bit inputs need K %% 8 == 0 and N %% 8 == 0 (TMA 16-byte strides)");
+        return VX_ERR_ALIGN;
+    }
+    if (desc->sm_count <= 0 || desc->smem_optin <= 0 || desc->tmem_cols <= 0 ||
+        desc->max_active_clusters[0] <= 0) {
+        set_error("invalid device descriptor"); return VX_ERR_INVALID;
+    }
+    std::unique_ptr<vx_plan_s> p(new (std::nothrow) vx_plan_s());
+    if (!p) return VX_ERR_OOM;
+    p->N = N; p->K = K; p->in = in; p->out = out; p->bl = bl; p->desc = *desc; p->device = -1;
+    vx_status st = build_rungs(p.get());
+    if (st != VX_OK) return st;
+    p->memo.resize(vx_plan_s::kMemo + 1);
+    p->memo_state.reset(new (std::nothrow) std::atomic<uint8_t>[vx_plan_s::kMemo + 1]);
+    if (!p->memo_state) return VX_ERR_OOM;
+    for (int64_t i = 0; i <= vx_plan_s::kMemo; ++i) p->memo_state[i].store(0);
+    *plan = p.release();
+    return VX_OK;
+}
+
+vx_status vx_plan(int64_t N, int64_t K, vx_dtype in, vx_dtype out, vx_blayout bl, int device,
+                  vx_plan_t* plan) {
+    vx_device_desc d;
+    vx_status st = vx_device_probe(device, &d);
+    if (st != VX_OK) return st;
+    st = vx_plan_ex(N, K, in, out, bl, &d, plan);
+    if (st != VX_OK) return st;
+    (*plan)->device = device;
+    st = prepare_kernels(*plan);
+    if (st != VX_OK) { vx_plan_destroy(*plan); *plan = nullptr; }
+    return st;
+}
+
+vx_status vx_plan_destroy(vx_plan_t plan) {
+    delete plan;
+    return VX_OK;
+}
+
+vx_status vx_plan_select(vx_plan_t plan, int64_t batch, int64_t M, int64_t N, vx_choice* out) {
+    return select_choice(plan, batch, M, N, -1, 0, out);
+}
+
+vx_status vx_plan_cost(vx_plan_t plan, int32_t rung_id, int32_t split, int64_t batch,
+                       int64_t M, int64_t N, vx_choice* out) {
+    if (rung_id < 0) { set_error("rung_id must be >= 0"); return VX_ERR_INVALID; }
+    return select_choice(plan, batch, M, N, rung_id, split, out);
+}
+
+vx_status vx_plan_dump(vx_plan_t p, char* buf, size_t cap, size_t* need) {
+    if (!p) { set_error("NULL plan"); return VX_ERR_INVALID; }
+    std::string s;
+    char tmp[512];
+    const Calib& c = calib_globals();
+    snprintf(tmp, sizeof tmp,
+             "{\"abi\":%d,\"N\":%lld,\"K\":%lld,\"in\":\"%s\",\"out\":\"%s\",\"b_layout\":\"%s\","
+             "\"levels\":{\"l0\":%lld,\"l1\":%lld,\"l2\":%lld,\"l3\":%lld},"
+             "\"calib\":{\"hbm_milli\":%lld,\"dsm_milli\":%lld,\"fixed_cluster\":%lld},\"rungs\":[",
+             VX_ABI_VERSION, (long long)p->N, (long long)p->K, dt_name(p->in), dt_name(p->out),
+             p->bl == VX_B_KN ? "kn" : "nk", (long long)p->counts.l0, (long long)p->counts.l1,
+             (long long)p->counts.l2, (long long)p->counts.l3, (long long)c.hbm_milli,
+             (long long)c.dsm_milli, (long long)c.fixed_cluster);
+    s += tmp;
+    for (size_t i = 0; i < p->rungs.size(); ++i) {
+        const Rung& r = p->rungs[i];
+        snprintf(tmp, sizeof tmp,
+                 "%s{\"rung_id\":%d,\"family\":%d,\"cg\":%d,\"um\":%d,\"un\":%d,\"acc_stages\":%d,"
+                 "\"bm\":%d,\"bn\":%d,\"bk\":%d,\"stages\":%d,\"swap\":%d,\"splits\":[",
+                 i ? "," : "", r.rung_id, r.family, r.cg, r.um, r.un, r.acc_stages, r.bm, r.bn,
+                 r.bk, r.stages, r.swap);
+        s += tmp;
+        for (size_t j = 0; j < r.splits.size(); ++j) {
+            snprintf(tmp, sizeof tmp, "%s%d", j ? "," : "", r.splits[j]);
+            s += tmp;
+        }
+        snprintf(tmp, sizeof tmp, "],\"mac_milli\":%lld,\"l2s_milli\":%lld,\"epi_milli\":%lld,\"fixed\":%lld}",
+                 (long long)r.mac_milli, (long long)r.l2s_milli, (long long)r.epi_milli, (long long)r.fixed);
+        s += tmp;
+    }
+    s += "]}";
+    if (need) *need = s.size() + 1;
+    if (!buf || cap < s.size() + 1) { set_error("dump buffer too small"); return VX_ERR_BUFFER; }
+    memcpy(buf, s.c_str(), s.size() + 1);
+    return VX_OK;
+}
+
+}  // extern "C"

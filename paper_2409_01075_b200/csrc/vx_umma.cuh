@@ -1,0 +1,347 @@
+// vx_umma.cuh -- the tcgen05 ladder kernel (families 0 "umma" and 1 "umma_swap").
+//
+// One template realises a rung of the strategy table on sm_100a.  The
+// paper's rKernel levels (Alg. 1; Table 1 GPU rows)
+// map to:
+//   L0  tcgen05.mma.cta_group::1.kind::f16, 128 x BN x 16, operands in SMEM, D in TMEM
+//   L1  TMEM accumulator tile 128 lanes x BN fp32 columns, double buffered (2 x BN cols)
+//   L2  CTA tile 128 x BN x 64: TMA (128-B swizzle) fills an S-stage SMEM ring -- the
+//       "Load" stage (GlobalMem -> SharedMem); TRL loop = the K loop over 64-wide blocks
+//   L3  grid: persistent CTAs over output tiles (PL loop), or a cluster of `splits` CTAs
+//       splitting the K loop and reducing through distributed shared memory.
+// Padding exists only at the grid level: TMA zero-fills rows/cols past M, N, K and the
+// epilogue masks stores past M and N (fig:padding).
+//
+// Operand naming inside the kernel: "P" is the operand on the UMMA-M axis (128 rows per
+// tile), "Q" the one on the UMMA-N axis (BN rows per tile).  family 0: P = A (rows of M),
+// Q = B (rows of N).  family 1 (swap): P = B (N), Q = A (M), so skinny M sits on the
+// narrow UMMA-N axis and N fills the 128-lane M axis (decode shapes).
+//
+// Warp roles (192 threads, one CTA per SM):
+//   warp 0      TMA producer (one lane)
+//   warp 1      TMEM allocator + MMA issuer (one lane issues every tcgen05.mma)
+//   warps 2..5  epilogue: tcgen05.ld TMEM -> registers -> global (warp w reads lanes
+//               32*(w%4) .. +31 of the accumulator)
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "vx_ptx.cuh"
+
+namespace vx {
+
+struct UmmaParams {
+    int M, N;                 // logical GEMM rows / cols (per batch)
+    int tiles_p, tiles_q;     // tiles along the UMMA-M (P) and UMMA-N (Q) axes
+    int num_tiles;            // batch * tiles_p * tiles_q
+    int kb_total;             // 64-wide K blocks
+    int splits;               // K-loop split (cluster size); 1 = persistent schedule
+    int stages;               // SMEM ring depth
+    int out_kind;             // 0 bf16, 1 fp16, 2 fp32
+    uint32_t idesc;           // tcgen05 instruction descriptor
+    void* C;
+    long long ldc;            // elements between rows of C
+    long long sC;             // elements between batches of C
+};
+
+constexpr int kEpiWarp0 = 2;
+constexpr int kThreads = 192;
+constexpr int kGroupP = 8;    // raster: 8 P-tiles x all Q-tiles per group (L2 reuse)
+
+template <int BN>
+struct UmmaCfg {
+    static constexpr int kPBytes = 128 * 64 * 2;
+    static constexpr int kQBytes = BN * 64 * 2;
+    static constexpr int kTmemCols = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
+                                   : (2 * BN <= 256) ? 256 : 512;
+};
+
+__device__ __forceinline__ void decode_tile(int tile, int tiles_p, int tiles_q, int& b, int& tp,
+                                            int& tq) {
+    const int per_b = tiles_p * tiles_q;
+    b = tile / per_b;
+    const int t = tile - b * per_b;
+    const int group = t / (kGroupP * tiles_q);
+    const int first = group * kGroupP;
+    const int gsz = min(kGroupP, tiles_p - first);
+    const int local = t - group * kGroupP * tiles_q;
+    tp = first + local % gsz;
+    tq = local / gsz;
+}
+
+__device__ __forceinline__ uint32_t pack2(float a, float b, int kind) {
+    if (kind == 0) {
+        __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+        return *reinterpret_cast<uint32_t*>(&h);
+    }
+    __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+}
+
+__device__ __forceinline__ void store1(void* C, long long idx, float v, int kind) {
+    if (kind == 2) {
+        reinterpret_cast<float*>(C)[idx] = v;
+    } else if (kind == 0) {
+        reinterpret_cast<__nv_bfloat16*>(C)[idx] = __float2bfloat16_rn(v);
+    } else {
+        reinterpret_cast<__half*>(C)[idx] = __float2half_rn(v);
+    }
+}
+
+// 8 consecutive columns of one row (n % 8 == 0, N % 8 == 0 -> all-or-nothing in N)
+__device__ __forceinline__ void store8(void* C, long long idx, const float* f, int kind) {
+    if (kind == 2) {
+        float4* p = reinterpret_cast<float4*>(reinterpret_cast<float*>(C) + idx);
+        p[0] = make_float4(f[0], f[1], f[2], f[3]);
+        p[1] = make_float4(f[4], f[5], f[6], f[7]);
+    } else {
+        uint4 u;
+        u.x = pack2(f[0], f[1], kind);
+        u.y = pack2(f[2], f[3], kind);
+        u.z = pack2(f[4], f[5], kind);
+        u.w = pack2(f[6], f[7], kind);
+        *reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(C) + idx) = u;
+    }
+}
+
+// 4 consecutive columns (split-K reduce path, n % 4 == 0)
+__device__ __forceinline__ void store4(void* C, long long idx, float4 v, int kind) {
+    if (kind == 2) {
+        *reinterpret_cast<float4*>(reinterpret_cast<float*>(C) + idx) = v;
+    } else {
+        uint2 u;
+        u.x = pack2(v.x, v.y, kind);
+        u.y = pack2(v.z, v.w, kind);
+        *reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(C) + idx) = u;
+    }
+}
+
+// SWAP: P = B, Q = A.  P_MN / Q_MN: that operand is MN-major in SMEM (B stored K x N).
+template <int BN, bool SWAP, bool P_MN, bool Q_MN>
+__global__ void __launch_bounds__(kThreads, 1)
+    vx_umma_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmQ,
+                   const UmmaParams p) {
+    using Cfg = UmmaCfg<BN>;
+    constexpr int kP = Cfg::kPBytes, kQ = Cfg::kQBytes;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int S = p.stages;
+
+    // layout: [barriers | pad to 1024 | S x P tiles | S x Q tiles]
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
+    uint64_t* empty = full + S;
+    uint64_t* tfull = empty + S;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+    const uint32_t raw_addr = ptx::smem_addr(smem_raw);
+    const uint32_t tile_off = ((raw_addr + 512 + 1023) & ~1023u) - raw_addr;
+    uint8_t* sP = smem_raw + tile_off;
+    uint8_t* sQ = sP + S * kP;
+
+    if (warp == 0 && lane == 0) {
+        ptx::prefetch_tmap(&tmP);
+        ptx::prefetch_tmap(&tmQ);
+        for (int i = 0; i < S; ++i) {
+            ptx::mbar_init(&full[i], 1);
+            ptx::mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            ptx::mbar_init(&tfull[i], 1);
+            ptx::mbar_init(&tempty[i], 4);
+        }
+        ptx::fence_mbar_init();
+    }
+    if (warp == 1) ptx::tmem_alloc<Cfg::kTmemCols>(tmem_holder);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_holder;
+
+    // work assignment: split mode -> one tile per cluster, K range by cluster rank;
+    // persistent mode -> tiles blockIdx.x, +gridDim.x, ...; whole K range
+    const bool split = p.splits > 1;
+    const int rank = split ? (int)(blockIdx.x % p.splits) : 0;
+    const int tile0 = split ? (int)(blockIdx.x / p.splits) : (int)blockIdx.x;
+    const int tstep = split ? p.num_tiles : (int)gridDim.x;
+    const int kb_n = p.kb_total / p.splits;
+    const int kb0 = rank * kb_n;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ===== TMA producer =====
+            const uint64_t pol = ptx::policy_evict_last();
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = tile0; tile < p.num_tiles; tile += tstep) {
+                int b, tp, tq;
+                decode_tile(tile, p.tiles_p, p.tiles_q, b, tp, tq);
+                for (int kb = kb0; kb < kb0 + kb_n; ++kb) {
+                    ptx::mbar_wait(&empty[stage], phase ^ 1);
+                    ptx::mbar_arrive_expect_tx(&full[stage], kP + kQ);
+                    uint8_t* dP = sP + stage * kP;
+                    uint8_t* dQ = sQ + stage * kQ;
+                    if (P_MN) {  // [64 K rows x 64 MN] atoms, 8 KB apart
+#pragma unroll
+                        for (int a = 0; a < 2; ++a)
+                            ptx::tma_load_3d(dP + a * 8192, &tmP, &full[stage], tp * 128 + a * 64,
+                                             kb * 64, b, pol);
+                    } else {
+                        ptx::tma_load_3d(dP, &tmP, &full[stage], kb * 64, tp * 128, b, pol);
+                    }
+                    if (Q_MN) {
+#pragma unroll
+                        for (int a = 0; a < BN / 64; ++a)
+                            ptx::tma_load_3d(dQ + a * 8192, &tmQ, &full[stage], tq * BN + a * 64,
+                                             kb * 64, b, pol);
+                    } else {
+                        ptx::tma_load_3d(dQ, &tmQ, &full[stage], kb * 64, tq * BN, b, pol);
+                    }
+                    if (++stage == S) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ===== MMA issuer (single thread) =====
+            int stage = 0;
+            uint32_t phase = 0;
+            int it = 0;
+            for (int tile = tile0; tile < p.num_tiles; tile += tstep, ++it) {
+                const int acc = it & 1;
+                const uint32_t acc_phase = (it >> 1) & 1;
+                ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * BN;
+                for (int i = 0; i < kb_n; ++i) {
+                    ptx::mbar_wait(&full[stage], phase);
+                    ptx::tc_fence_after();
+                    const uint32_t aP = ptx::smem_addr(sP + stage * kP);
+                    const uint32_t aQ = ptx::smem_addr(sQ + stage * kQ);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        // K-major: +32 B inside the swizzle row; MN-major: +2 K-groups (2 KB)
+                        const uint64_t dp = P_MN ? ptx::sdesc_mn_sw128(aP + k * 2048, 8192)
+                                                 : ptx::sdesc_k_sw128(aP + k * 32);
+                        const uint64_t dq = Q_MN ? ptx::sdesc_mn_sw128(aQ + k * 2048, 8192)
+                                                 : ptx::sdesc_k_sw128(aQ + k * 32);
+                        ptx::umma_f16(d_tmem, dp, dq, p.idesc, (i | k) != 0);
+                    }
+                    ptx::umma_commit(&empty[stage]);  // frees the stage when these MMAs finish
+                    if (++stage == S) { stage = 0; phase ^= 1; }
+                }
+                ptx::umma_commit(&tfull[acc]);        // accumulator ready for the epilogue
+            }
+        }
+    } else {
+        // ===== epilogue warps =====
+        const int quarter = warp & 3;
+        const int row = quarter * 32 + lane;  // accumulator lane = row of the P tile
+        float* red = reinterpret_cast<float*>(sP);  // split mode: reuse the drained ring
+        constexpr int RS = BN + 4;                  // padded row stride (floats)
+        int it = 0;
+        for (int tile = tile0; tile < p.num_tiles; tile += tstep, ++it) {
+            int b, tp, tq;
+            decode_tile(tile, p.tiles_p, p.tiles_q, b, tp, tq);
+            const int acc = it & 1;
+            const uint32_t acc_phase = (it >> 1) & 1;
+            ptx::mbar_wait(&tfull[acc], acc_phase);
+            ptx::tc_fence_after();
+            const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
+            const int pr = tp * 128 + row;  // global index on the P axis
+            char* Cb = reinterpret_cast<char*>(p.C) +
+                       (long long)b * p.sC * (p.out_kind == 2 ? 4 : 2);
+#pragma unroll
+            for (int c = 0; c < (BN + 31) / 32; ++c) {
+                uint32_t v[32];
+                if (BN >= 32) ptx::tmem_ld32(taddr + c * 32, v);
+                else ptx::tmem_ld16(taddr + c * 32, v);
+                ptx::tmem_wait_ld();
+                constexpr int W = BN >= 32 ? 32 : BN;
+                const float* f = reinterpret_cast<const float*>(v);
+                if (split) {
+#pragma unroll
+                    for (int j = 0; j < W; j += 4)
+                        *reinterpret_cast<float4*>(&red[row * RS + c * 32 + j]) =
+                            make_float4(f[j], f[j + 1], f[j + 2], f[j + 3]);
+                } else if (!SWAP) {
+                    // row pr = m, columns = n
+                    if (pr < p.M) {
+                        const long long base = (long long)pr * p.ldc;
+#pragma unroll
+                        for (int j = 0; j < W; j += 8) {
+                            const int n = tq * BN + c * 32 + j;
+                            if (n < p.N) store8(Cb, base + n, f + j, p.out_kind);
+                        }
+                    }
+                } else {
+                    // row pr = n, columns = m
+                    if (pr < p.N) {
+#pragma unroll
+                        for (int j = 0; j < W; ++j) {
+                            const int m = tq * BN + c * 32 + j;
+                            if (m < p.M) store1(Cb, (long long)m * p.ldc + pr, f[j], p.out_kind);
+                        }
+                    }
+                }
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+        }
+    }
+
+    __syncwarp();  // reconverge the single-lane roles before the .aligned cluster barriers
+    if (split) {
+        // deterministic in-cluster reduction: CTA `rank` owns rows [rank*128/s, +128/s) of
+        // the tile and sums the s partials in rank order 0..s-1 through DSMEM
+        ptx::cluster_sync();
+        if (warp >= kEpiWarp0) {
+            int b, tp, tq;
+            decode_tile(tile0, p.tiles_p, p.tiles_q, b, tp, tq);
+            constexpr int RS = BN + 4;
+            const int rows = 128 / p.splits;
+            const int r0 = rank * rows;
+            const int et = threadIdx.x - kEpiWarp0 * 32;
+            const uint32_t red_addr = ptx::smem_addr(sP);
+            char* Cb = reinterpret_cast<char*>(p.C) +
+                       (long long)b * p.sC * (p.out_kind == 2 ? 4 : 2);
+            const int n4 = BN / 4;
+            for (int idx = et; idx < rows * n4; idx += 128) {
+                int rr, cc;
+                if (SWAP) { rr = idx % rows; cc = (idx / rows) * 4; }   // consecutive n
+                else { rr = idx / n4; cc = (idx % n4) * 4; }            // consecutive n
+                const int row = r0 + rr;
+                const uint32_t off = (uint32_t)(row * RS + cc) * 4u;
+                float4 acc4 = ptx::ld_dsmem_f4(ptx::mapa(red_addr + off, 0));
+                for (int j = 1; j < p.splits; ++j) {
+                    float4 t = ptx::ld_dsmem_f4(ptx::mapa(red_addr + off, j));
+                    acc4.x += t.x; acc4.y += t.y; acc4.z += t.z; acc4.w += t.w;
+                }
+                const int pr = tp * 128 + row;
+                const int q0 = tq * BN + cc;
+                if (!SWAP) {
+                    if (pr < p.M && q0 < p.N) store4(Cb, (long long)pr * p.ldc + q0, acc4, p.out_kind);
+                } else if (pr < p.N) {
+                    const float e[4] = {acc4.x, acc4.y, acc4.z, acc4.w};
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        if (q0 + j < p.M) store1(Cb, (long long)(q0 + j) * p.ldc + pr, e[j], p.out_kind);
+                }
+            }
+        }
+        ptx::cluster_sync();
+    }
+
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        __syncwarp();
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+    }
+}
+
+}  // namespace vx
