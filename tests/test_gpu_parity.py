@@ -1,0 +1,233 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the fp64 oracle, element by element.
+
+Bars (BASELINE.json north_star):
+  * integer inputs ({-2..2}): every partial sum is an exact small integer, so any fp32
+    accumulation order is exact -> C must EQUAL the oracle (fp32 out) or RNE(oracle)
+    (bf16/fp16 out), for every rung x split x tail;
+  * N(0,1)/N(0,1/K) inputs: max|C - C_ref| <= 2e-2*sqrt(K/4096)*max|C_ref| (bf16/fp16 in,
+    fp32 out); bf16/fp16 output adds the output rounding, 2^-8 (bf16) / 2^-11 (fp16)
+    of |C_ref| per element (reading R12);
+  * fp32 path: max|C - C_ref| <= 1e-5*max|C_ref| (reading R12).
+Full BASELINE sizes are checked on sampled rows (first, last, last partial tile, random).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def vxmod():
+    import paper_2409_01075_b200 as vx
+    return vx
+
+
+def _round_to(ref: np.ndarray, out: str) -> np.ndarray:
+    t = torch.from_numpy(ref)
+    if out == "bf16":
+        return t.float().to(torch.bfloat16).double().numpy()   # exact ints < 2^24 -> one RNE
+    if out == "fp16":
+        return t.float().to(torch.float16).double().numpy()
+    return ref
+
+
+def _tol(ref, K, out):
+    base = 2e-2 * np.sqrt(K / 4096.0) * np.abs(ref).max()
+    rel = {"bf16": 2.0 ** -8, "fp16": 2.0 ** -11, "fp32": 0.0}[out]
+    return base + rel * np.abs(ref)
+
+
+def _run(p, A, B, force=None):
+    C, ch = p.gemm(A.cuda(), B.cuda(), force=force, want_choice=True)
+    torch.cuda.synchronize()
+    return C.cpu().double().numpy(), ch
+
+
+@pytest.mark.parametrize("bl", ["nk", "kn"])
+@pytest.mark.parametrize("out", ["fp32", "bf16"])
+def test_every_rung_and_split_integer_exact(bl, out):
+    vx = vxmod()
+    N, K = 384, 512                       # N tail for BN=256, 8 k-blocks (splits 1..8)
+    p = vx.Plan(N, K, "bf16", out, bl)
+    for M in (1, 17, 128, 129, 333):      # single row, sub-tile, exact tile, ragged tails
+        A, B = synth.gemm_inputs(M, N, K, "bf16", bl, kind="int", seed=100 + M)
+        want = _round_to(oracle.gemm(A, B, bl), out)
+        for r in p.dump()["rungs"]:
+            for s in r["splits"]:
+                got, ch = _run(p, A, B, force=(r["rung_id"], s))
+                assert ch["rung_id"] == r["rung_id"] and ch["split"] == s
+                assert np.array_equal(got, want), (M, r, s, np.abs(got - want).max())
+
+
+def test_fp16_inputs_integer_exact():
+    vx = vxmod()
+    N, K = 256, 320                       # K not a multiple of 64: TMA zero-fills the K tail
+    p = vx.Plan(N, K, "fp16", "fp16", "nk")
+    for M in (5, 200):
+        A, B = synth.gemm_inputs(M, N, K, "fp16", "nk", kind="int", seed=M)
+        want = _round_to(oracle.gemm(A, B, "nk"), "fp16")
+        for r in p.dump()["rungs"]:
+            for s in r["splits"]:
+                got, _ = _run(p, A, B, force=(r["rung_id"], s))
+                assert np.array_equal(got, want), (M, r["rung_id"], s)
+
+
+@pytest.mark.parametrize("bl", ["nk", "kn"])
+def test_random_tolerance_selected(bl):
+    vx = vxmod()
+    for (N, K) in ((768, 768), (2304, 768)):
+        p = vx.Plan(N, K, "bf16", "fp32", bl)
+        for M in (1, 3, 64, 100, 513, 1000):
+            A, B = synth.gemm_inputs(M, N, K, "bf16", bl, kind="normal", seed=M)
+            ref = oracle.gemm(A, B, bl)
+            got, ch = _run(p, A, B)
+            assert ch == p.select(M) | {}, "launched decision differs from the selector"
+            assert np.all(np.abs(got - ref) <= _tol(ref, K, "fp32")), (N, K, M, ch)
+
+
+def test_bf16_out_tolerance():
+    vx = vxmod()
+    N, K = 3072, 768
+    p = vx.Plan(N, K, "bf16", "bf16", "nk")
+    for M in (7, 512, 2000):
+        A, B = synth.gemm_inputs(M, N, K, "bf16", "nk", kind="normal", seed=M)
+        ref = oracle.gemm(A, B, "nk")
+        got, _ = _run(p, A, B)
+        assert np.all(np.abs(got - ref) <= _tol(ref, K, "bf16"))
+
+
+def _sample_rows(M, bm=128, n_rand=24, seed=0):
+    rows = set(range(min(4, M))) | set(range(max(0, M - 4), M))
+    last_tile = (M - 1) // bm * bm
+    rows |= set(range(last_tile, M, max(1, (M - last_tile) // 8)))
+    rng = np.random.default_rng(seed)
+    rows |= set(rng.integers(0, M, size=n_rand).tolist())
+    return sorted(rows)
+
+
+@pytest.mark.parametrize("N", [4096, 11008, 12288])
+def test_llama_full_size_sampled_rows(N):
+    vx = vxmod()
+    K = 4096
+    p = vx.Plan(N, K, "bf16", "bf16", "nk")
+    for M in (1, 16, 64, 129, 512, 4096, 16384):
+        A, B = synth.gemm_inputs(M, N, K, "bf16", "nk", kind="normal", seed=M,
+                                 device="cuda")
+        C, ch = p.gemm(A, B, want_choice=True)
+        torch.cuda.synchronize()
+        rows = _sample_rows(M, n_rand=8)
+        ref = oracle.gemm(A[rows].cpu(), B.cpu(), "nk")
+        got = C[rows].double().cpu().numpy()
+        assert np.all(np.abs(got - ref) <= _tol(ref, K, "bf16")), (N, M, ch)
+
+
+def test_bert_full_size_sampled_rows():
+    vx = vxmod()
+    K = 768
+    for N in (768, 2304, 3072):
+        p = vx.Plan(N, K, "bf16", "bf16", "nk")
+        for M in (1, 37, 476, 1000, 4096):
+            A, B = synth.gemm_inputs(M, N, K, "bf16", "nk", kind="normal", seed=M,
+                                     device="cuda")
+            C = p.gemm(A, B)
+            torch.cuda.synchronize()
+            rows = _sample_rows(M, n_rand=16)
+            ref = oracle.gemm(A[rows].cpu(), B.cpu(), "nk")
+            got = C[rows].double().cpu().numpy()
+            assert np.all(np.abs(got - ref) <= _tol(ref, K, "bf16")), (N, M)
+
+
+def test_pad_poisoning():
+    """Rows past M of A are NaN and C is over-allocated with a sentinel: nothing leaks."""
+    vx = vxmod()
+    N, K = 512, 256
+    p = vx.Plan(N, K, "bf16", "fp32", "nk")
+    for M in (1, 100, 130):
+        A, B = synth.gemm_inputs(M, N, K, "bf16", "nk", kind="int", seed=3)
+        Abig = torch.full((M + 200, K), float("nan"), dtype=torch.bfloat16, device="cuda")
+        Abig[:M] = A.cuda()
+        Cbig = torch.full((M + 64, N), 12345.0, dtype=torch.float32, device="cuda")
+        want = oracle.gemm(A, B, "nk")
+        Bd = B.cuda()
+        for r in p.dump()["rungs"]:
+            for s in r["splits"]:
+                Cbig.fill_(12345.0)
+                vx.lib.vx_gemm_ex(p.handle, 1, M, N, K, Abig.data_ptr(), M * K, Bd.data_ptr(),
+                                  N * K, Cbig.data_ptr(), M * N, r["rung_id"], s, None, None)
+                torch.cuda.synchronize()
+                got = Cbig.cpu().double().numpy()
+                assert np.array_equal(got[:M], want)
+                assert np.all(got[M:] == 12345.0)
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_batched_attention_scores(d):
+    vx = vxmod()
+    p = vx.Plan(0, d, "bf16", "fp32", "nk")
+    batch = 4
+    for s in (1, 7, 100, 257):
+        Q, Kt = synth.gemm_inputs(s, s, d, "bf16", "nk", kind="int", seed=s, batch=batch)
+        want = oracle.gemm(Q, Kt, "nk")
+        got, ch = _run(p, Q, Kt)
+        assert np.array_equal(got, want), (d, s, ch)
+        for r in p.dump()["rungs"]:
+            got, _ = _run(p, Q, Kt, force=(r["rung_id"], r["splits"][-1]))
+            assert np.array_equal(got, want), (d, s, r)
+
+
+def test_batched_attention_full_size_sampled():
+    vx = vxmod()
+    for d in (64, 128):
+        p = vx.Plan(0, d, "bf16", "bf16", "nk")
+        s = 2048
+        Q, Kt = synth.gemm_inputs(s, s, d, "bf16", "nk", kind="normal", seed=d, batch=32,
+                                  device="cuda")
+        C = p.gemm(Q, Kt)
+        torch.cuda.synchronize()
+        for b in (0, 17, 31):
+            rows = _sample_rows(s, n_rand=4, seed=b)
+            ref = oracle.gemm(Q[b, rows].cpu(), Kt[b].cpu(), "nk")
+            got = C[b, rows].double().cpu().numpy()
+            assert np.all(np.abs(got - ref) <= _tol(ref, d, "bf16"))
+
+
+def test_fp32_simt_path():
+    vx = vxmod()
+    for bl in ("nk", "kn"):
+        p = vx.Plan(64, 64, "fp32", "fp32", bl)
+        for M in (1, 37, 200):
+            A, B = synth.gemm_inputs(M, 64, 64, "fp32", bl, kind="normal", seed=M)
+            ref = oracle.gemm(A, B, bl)
+            for r in p.dump()["rungs"]:
+                got, ch = _run(p, A, B, force=(r["rung_id"], 1))
+                assert np.abs(got - ref).max() <= 1e-5 * np.abs(ref).max(), (bl, M, r)
+    # config 1 exactly: M=37, N=64, K=64 via the selector
+    p = vx.Plan(64, 64, "fp32", "fp32", "kn")
+    A, B = synth.gemm_inputs(37, 64, 64, "fp32", "kn", kind="normal", seed=1)
+    ref = oracle.gemm(A, B, "kn")
+    got, _ = _run(p, A, B)
+    assert np.abs(got - ref).max() <= 1e-5 * np.abs(ref).max()
+
+
+def test_m_zero_and_errors():
+    vx = vxmod()
+    p = vx.Plan(256, 256, "bf16", "bf16", "nk")
+    A = torch.zeros(0, 256, dtype=torch.bfloat16, device="cuda")
+    B = torch.zeros(256, 256, dtype=torch.bfloat16, device="cuda")
+    C = p.gemm(A, B)
+    assert C.shape == (0, 256)
+    with pytest.raises(ValueError):
+        p.gemm(torch.zeros(4, 256, dtype=torch.float16, device="cuda"), B)
+
+
+def test_device_descriptor_matches_golden():
+    """The captured descriptor the CPU selector tests use is this device's."""
+    import json, os
+    vx = vxmod()
+    d = vx.device_probe(0).to_json()
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "b200_desc.json")))
+    for k in ("sm_count", "smem_optin", "max_active_clusters", "tmem_cols"):
+        assert d[k] == g[k], k

@@ -1,0 +1,106 @@
+"""Library strategy table + runtime selection vs the independent oracle (CPU only).
+
+north_star: "GPU tile selection must match the CPU selector bit-exact for every M in
+1..16384".  The library's selector is host code, so it is compared here on the captured
+B200 descriptor (tests/golden/b200_desc.json) for every BASELINE (N, K), plus the
+dynamic-N batched attention plan for every s in 1..2048.
+"""
+import json
+import os
+
+import pytest
+
+import paper_2409_01075_b200 as vx
+from oracle import selector_ref as S
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+DESC_J = S.load_descriptor()
+CAL = S.load_calib()
+DESC = vx.DeviceDesc.from_json(DESC_J)
+
+BASELINE_NK = [(768, 768), (2304, 768), (3072, 768), (4096, 4096), (11008, 4096),
+               (12288, 4096)]
+FIELDS = ("rung_id", "split", "tiles_m", "tiles_n", "grid", "cost")
+
+
+def _oracle_table(K, i, o):
+    return S.build_table(K, i, o, DESC_J)
+
+
+def _lib_rungs(dump):
+    keep = ("rung_id", "family", "cg", "um", "un", "acc_stages", "bm", "bn", "bk", "stages",
+            "swap", "splits")
+    return [{k: r[k] for k in keep} for r in dump["rungs"]]
+
+
+@pytest.mark.parametrize("K", [768, 4096, 64, 128, 2304])
+@pytest.mark.parametrize("io", [("bf16", "bf16"), ("fp16", "fp32"), ("fp32", "fp32")])
+def test_tables_identical(K, io):
+    p = vx.Plan(0, K, io[0], io[1], "nk", desc=DESC)
+    d = p.dump()
+    t = _oracle_table(K, io[0], io[1])
+    assert d["levels"] == t["levels"]
+    want = [{k: r[k] for k in ("rung_id", "family", "cg", "um", "un", "acc_stages", "bm", "bn",
+                               "bk", "stages", "swap", "splits")} for r in t["rungs"]]
+    assert _lib_rungs(d) == want
+
+
+def test_calibration_copies_agree():
+    d = vx.Plan(4096, 4096, "bf16", "bf16", "nk", desc=DESC).dump()
+    assert d["calib"] == {k: CAL[k] for k in ("hbm_milli", "dsm_milli", "fixed_cluster")}
+    for r in d["rungs"]:
+        key = "%s_%dx%d" % (S.FAMILY_NAMES[r["family"]], r["bm"], r["bn"])
+        for f in ("mac_milli", "l2s_milli", "epi_milli", "fixed"):
+            assert r[f] == CAL["rungs"][key][f], (key, f)
+    d = vx.Plan(64, 64, "fp32", "fp32", "nk", desc=DESC).dump()
+    for r in d["rungs"]:
+        key = "simt_%dx%d" % (r["bm"], r["bn"])
+        for f in ("mac_milli", "l2s_milli", "epi_milli", "fixed"):
+            assert r[f] == CAL["rungs"][key][f], (key, f)
+
+
+@pytest.mark.parametrize("N,K", BASELINE_NK)
+def test_select_every_M_bit_exact(N, K):
+    p = vx.Plan(N, K, "bf16", "bf16", "nk", desc=DESC)
+    t = _oracle_table(K, "bf16", "bf16")
+    for M in range(1, 16385):
+        a = p.select(M)
+        b = S.select(t, 1, M, N, K, DESC_J, CAL)
+        if tuple(a[f] for f in FIELDS) != tuple(b[f] for f in FIELDS):
+            pytest.fail("M=%d lib=%s oracle=%s" % (M, a, b))
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_select_batched_attention_every_s(d):
+    p = vx.Plan(0, d, "bf16", "bf16", "nk", desc=DESC)
+    t = _oracle_table(d, "bf16", "bf16")
+    for s in range(1, 2049):
+        a = p.select(s, N=s, batch=32)
+        b = S.select(t, 32, s, s, d, DESC_J, CAL)
+        assert tuple(a[f] for f in FIELDS) == tuple(b[f] for f in FIELDS), s
+
+
+def test_select_fp32_and_large_M():
+    p = vx.Plan(64, 64, "fp32", "fp32", "nk", desc=DESC)
+    t = _oracle_table(64, "fp32", "fp32")
+    for M in (1, 36, 37, 38, 1000, 65536):
+        a = p.select(M)
+        b = S.select(t, 1, M, 64, 64, DESC_J, CAL)
+        assert tuple(a[f] for f in FIELDS) == tuple(b[f] for f in FIELDS)
+    p = vx.Plan(11008, 4096, "bf16", "bf16", "nk", desc=DESC)
+    t = _oracle_table(4096, "bf16", "bf16")
+    for M in (16385, 32768, 65536, 65536 // 8, 65536 // 2, 100000):   # beyond the memo
+        a = p.select(M)
+        b = S.select(t, 1, M, 11008, 4096, DESC_J, CAL)
+        assert tuple(a[f] for f in FIELDS) == tuple(b[f] for f in FIELDS)
+
+
+def test_forced_cost_matches_oracle():
+    p = vx.Plan(3072, 768, "bf16", "bf16", "nk", desc=DESC)
+    t = _oracle_table(768, "bf16", "bf16")
+    for r in t["rungs"]:
+        for s in r["splits"]:
+            for M in (1, 77, 512, 4096):
+                a = p.cost(r["rung_id"], s, M)
+                b = S.rung_cost(r, s, 1, M, 3072, 768, "bf16", "bf16", DESC_J, CAL)
+                assert a["cost"] == b["cost"] and a["grid"] == b["grid"]
