@@ -17,6 +17,7 @@
 namespace vx {
 
 static std::atomic<int64_t> g_launches{0};
+static unsigned long long* g_trace = nullptr;  // device buffer, 8 x u64 per CTA (debug)
 
 // ---- instantiated kernels (the "implemented" filter of the strategy table, R6) -----------
 bool kernel_available(int family, int bm, int bn) {
@@ -192,6 +193,10 @@ vx_status launch(const vx_plan_s* p, const vx_choice& ch, int64_t batch, int64_t
     prm.C = C;
     prm.ldc = N;
     prm.sC = batch > 1 ? sC : M * N;
+    prm.trace = g_trace;
+    const int ob = p->out == VX_FP32 ? 4 : 2;
+    prm.vec = (N % 8 == 0) && ((prm.sC * ob) % 16 == 0) &&
+              ((reinterpret_cast<uintptr_t>(C) & 15) == 0);
 
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)ch.grid, 1, 1);
@@ -244,9 +249,14 @@ static vx_status check_args(const vx_plan_s* p, int64_t batch, int64_t M, int64_
     if (batch > 1 && (sA < M * K || sB < N * K || sC < M * N)) { set_error("batch strides overlap"); return VX_ERR_INVALID; }
     if (M > 0x7fffffffLL || N > 0x7fffffffLL) { set_error("M, N must fit in int32"); return VX_ERR_INVALID; }
     if (p->in != VX_FP32) {
-        if (N % 8 || K % 8) { set_error("16-bit inputs need N %% 8 == 0 and K %% 8 == 0"); return VX_ERR_ALIGN; }
-        if (!aligned16(A) || !aligned16(B) || !aligned16(C)) { set_error("operands must be 16-byte aligned"); return VX_ERR_ALIGN; }
-        if (batch > 1 && (sA % 8 || sB % 8 || sC % 8)) { set_error("batch strides must be multiples of 8 elements"); return VX_ERR_ALIGN; }
+        // TMA: 16-byte aligned bases and row / batch strides of A and B.  C is written with
+        // plain stores (vectorised only when aligned), so it has no alignment rule.
+        if (K % 8) { set_error("16-bit inputs need K %% 8 == 0"); return VX_ERR_ALIGN; }
+        if (p->bl == VX_B_KN && N % 8) { set_error("B stored K x N needs N %% 8 == 0"); return VX_ERR_ALIGN; }
+        if (!aligned16(A) || !aligned16(B)) { set_error("A and B must be 16-byte aligned"); return VX_ERR_ALIGN; }
+        if (batch > 1 && (sA % 8 || sB % 8)) { set_error("A/B batch strides must be multiples of 8 elements"); return VX_ERR_ALIGN; }
+        const int ob = p->out == VX_FP32 ? 4 : 2;
+        if (reinterpret_cast<uintptr_t>(C) % ob) { set_error("C must be element aligned"); return VX_ERR_ALIGN; }
     }
     return VX_OK;
 }
@@ -351,5 +361,9 @@ vx_status vx_gemm_host(vx_plan_t p, int64_t batch, int64_t M, int64_t N, int64_t
 }
 
 int64_t vx_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+/* Debug/tracing hook (not part of vx.h): subsequent tcgen05 launches write %globaltimer
+ * stamps of 8 phases per CTA into `buf` (device, >= 8*grid u64); NULL disables. */
+void vx_debug_set_trace(void* buf) { g_trace = reinterpret_cast<unsigned long long*>(buf); }
 
 }  // extern "C"

@@ -337,8 +337,8 @@ vx_status vx_plan_ex(int64_t N, int64_t K, vx_dtype in, vx_dtype out, vx_blayout
         set_error("bad dtype or layout enum"); return VX_ERR_INVALID;
     }
     if (in == VX_FP32 && out != VX_FP32) { set_error("fp32 inputs need fp32 output"); return VX_ERR_UNSUPPORTED; }
-    if (in != VX_FP32 && (K % 8 != 0 || (N > 0 && N % 8 != 0))) {
-        set_error("16-bit inputs need K %% 8 == 0 and N %% 8 == 0 (TMA 16-byte strides)");
+    if (in != VX_FP32 && (K % 8 != 0 || (bl == VX_B_KN && N > 0 && N % 8 != 0))) {
+        set_error("16-bit inputs need K %% 8 == 0 (and N %% 8 == 0 when B is K x N): TMA 16-byte strides");
         return VX_ERR_ALIGN;
     }
     if (desc->sm_count <= 0 || desc->smem_optin <= 0 || desc->tmem_cols <= 0 ||

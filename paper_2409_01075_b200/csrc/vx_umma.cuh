@@ -39,11 +39,22 @@ struct UmmaParams {
     int splits;               // K-loop split (cluster size); 1 = persistent schedule
     int stages;               // SMEM ring depth
     int out_kind;             // 0 bf16, 1 fp16, 2 fp32
+    int vec;                  // 1: C rows/batches 16-B aligned and N % 8 == 0 (vector stores)
     uint32_t idesc;           // tcgen05 instruction descriptor
     void* C;
     long long ldc;            // elements between rows of C
     long long sC;             // elements between batches of C
+    unsigned long long* trace;  // optional per-CTA phase timestamps (VX_TRACE), else null
 };
+
+// phase trace (tracing aux subsystem): %globaltimer (ns) at fixed points, 8 slots per CTA
+__device__ __forceinline__ void trace_at(const UmmaParams& p, int slot) {
+    if (p.trace) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        p.trace[blockIdx.x * 8 + slot] = t;
+    }
+}
 
 constexpr int kEpiWarp0 = 2;
 constexpr int kThreads = 192;
@@ -129,6 +140,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int S = p.stages;
+    if (threadIdx.x == 0) trace_at(p, 0);
 
     // layout: [barriers | pad to 1024 | S x P tiles | S x Q tiles]
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
@@ -159,6 +171,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
+    if (threadIdx.x == 0) trace_at(p, 1);
 
     // work assignment: split mode -> one tile per cluster, K range by cluster rank;
     // persistent mode -> tiles blockIdx.x, +gridDim.x, ...; whole K range
@@ -202,6 +215,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (++stage == S) { stage = 0; phase ^= 1; }
                 }
             }
+            trace_at(p, 2);
         }
     } else if (warp == 1) {
         if (lane == 0) {
@@ -218,6 +232,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int i = 0; i < kb_n; ++i) {
                     ptx::mbar_wait(&full[stage], phase);
                     ptx::tc_fence_after();
+                    if (it == 0 && i == 0) trace_at(p, 3);
                     const uint32_t aP = ptx::smem_addr(sP + stage * kP);
                     const uint32_t aQ = ptx::smem_addr(sQ + stage * kQ);
 #pragma unroll
@@ -234,6 +249,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 ptx::umma_commit(&tfull[acc]);        // accumulator ready for the epilogue
             }
+            trace_at(p, 4);
         }
     } else {
         // ===== epilogue warps =====
@@ -249,6 +265,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t acc_phase = (it >> 1) & 1;
             ptx::mbar_wait(&tfull[acc], acc_phase);
             ptx::tc_fence_after();
+            if (it == 0 && threadIdx.x == kEpiWarp0 * 32) trace_at(p, 5);
             const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
             const int pr = tp * 128 + row;  // global index on the P axis
             char* Cb = reinterpret_cast<char*>(p.C) +
@@ -273,7 +290,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                         for (int j = 0; j < W; j += 8) {
                             const int n = tq * BN + c * 32 + j;
-                            if (n < p.N) store8(Cb, base + n, f + j, p.out_kind);
+                            if (p.vec) {
+                                if (n < p.N) store8(Cb, base + n, f + j, p.out_kind);
+                            } else {
+#pragma unroll
+                                for (int e = 0; e < 8; ++e)
+                                    if (n + e < p.N) store1(Cb, base + n + e, f[j + e], p.out_kind);
+                            }
                         }
                     }
                 } else {
@@ -294,6 +317,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 
     __syncwarp();  // reconverge the single-lane roles before the .aligned cluster barriers
+    if (threadIdx.x == kEpiWarp0 * 32) trace_at(p, 6);
     if (split) {
         // deterministic in-cluster reduction: CTA `rank` owns rows [rank*128/s, +128/s) of
         // the tile and sums the s partials in rank order 0..s-1 through DSMEM
@@ -323,7 +347,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int pr = tp * 128 + row;
                 const int q0 = tq * BN + cc;
                 if (!SWAP) {
-                    if (pr < p.M && q0 < p.N) store4(Cb, (long long)pr * p.ldc + q0, acc4, p.out_kind);
+                    if (pr < p.M) {
+                        if (p.vec) {
+                            if (q0 < p.N) store4(Cb, (long long)pr * p.ldc + q0, acc4, p.out_kind);
+                        } else {
+                            const float e[4] = {acc4.x, acc4.y, acc4.z, acc4.w};
+#pragma unroll
+                            for (int j = 0; j < 4; ++j)
+                                if (q0 + j < p.N) store1(Cb, (long long)pr * p.ldc + q0 + j, e[j], p.out_kind);
+                        }
+                    }
                 } else if (pr < p.N) {
                     const float e[4] = {acc4.x, acc4.y, acc4.z, acc4.w};
 #pragma unroll
@@ -337,6 +370,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     ptx::tc_fence_before();
     __syncthreads();
+    if (threadIdx.x == 0) trace_at(p, 7);
     if (warp == 1) {
         __syncwarp();
         ptx::tc_fence_after();
