@@ -9,10 +9,11 @@ N in {768,2304,3072}) and LLaMA-7B (K=4096, N in {4096,11008,12288}) linear laye
 the SURVEY 8(d) d2 M sweeps (192 points), bf16 in / fp32 accumulate / bf16 out, B as an
 [N,K] weight.  One STEP = one vx_gemm call (selection + launch) per sweep point.
 
-Timing: per point, R rotating (A, B, C) buffer sets whose total exceeds 3x L2 are launched
-back-to-back (one vx_gemm each, selection + tensor maps done at CUDA-graph capture); CUDA
-events bracket each point's graph replay on the launching stream; per-launch time = graph
-time / R, median over the K timed steps (max over ranks for N > 1).  value = geomean over points of TFLOP/s (x N ranks: each rank
+Timing: per point, 4 back-to-back vx_gemm launches on fresh slices of >= 1 GiB operand
+arenas (cold L2: a slice is reused only after the arena wraps), captured in a CUDA graph
+(selection + tensor maps at capture); CUDA events bracket each point's graph replay on the
+launching stream; per-launch time = graph time / 4, median over the K timed steps (max
+over ranks for N > 1).  value = geomean over points of TFLOP/s (x N ranks: each rank
 runs its own copy of the sweep -> weak scaling; no data-path collective).  The M=65536
 LLaMA FFN of configs[4] is additionally run row-sharded across the N ranks ("sharded").
 
@@ -237,34 +238,50 @@ def workload_config():
                         "LLaMA-7B (K=4096, N in {4096,11008,12288}) linear layers, dynamic M "
                         "sweep (SURVEY 8(d) d2), B as [N,K] weight",
             "points": len(sweep_points()), "in": "bf16", "out": "bf16", "accumulate": "fp32",
-            "l2": "operands cold: per point, R rotating (A,B,C) sets moving > 3x L2 per pass, "
-                  "launched back-to-back from a CUDA graph; per-launch time = graph time / R",
+            "l2": "operands cold: every launch takes fresh slices of >= 1 GiB A/B/C arenas "
+                  "(reuse only after the arena wraps, ~8x L2); 4 launches per point per "
+                  "step, back-to-back from a CUDA graph; per-launch time = graph time / 4",
             "sharded": "configs[4]: M=65536, N=11008, K=4096 row-sharded over n_gpus"}
 
 
 # ----------------------------------------------------------------------------------------
 # the product arm
 # ----------------------------------------------------------------------------------------
-RMAX = 512
+R_PER_POINT = 4
 
 
-def rotation(M, N, K, l2_bytes, batch=1, rmax=None):
-    """Buffer sets per point: enough distinct (A, B, C) sets that one pass over them moves
-    more than 3x L2, so every launch reads cold operands (timing rule)."""
-    set_bytes = 2 * batch * (M * K + N * K + M * N)
-    return int(min(rmax or RMAX, max(4, -(-3 * l2_bytes // set_bytes))))
+class Arena:
+    """A large device buffer handed out in rolling slices.  Consecutive launches take
+    consecutive slices and wrap around, so a slice is reused only after the whole arena
+    (>= 1 GiB, ~8x L2) has been streamed through: every launch reads cold operands."""
+
+    def __init__(self, n_elems, dev, kind, seed, scale=1.0):
+        if kind == "empty":
+            self.t = torch.empty(n_elems, dtype=torch.bfloat16, device=dev)
+        else:
+            self.t = synth.matrix((n_elems,), "bf16", kind, seed=seed, scale=scale, device=dev)
+        self.n = n_elems
+        self.pos = 0
+
+    def take(self, n):
+        assert n <= self.n
+        if self.pos + n > self.n:
+            self.pos = 0
+        p = self.t[self.pos:].data_ptr()
+        self.pos += (n + 127) // 128 * 128     # keep 256-B alignment
+        return p
 
 
 class PointGraph:
-    """R back-to-back vx_gemm launches over rotating buffer sets, captured in a CUDA graph
-    (selection + tensor-map encoding happen at capture; replay re-issues the kernels)."""
+    """R back-to-back vx_gemm launches of one sweep point on fresh arena slices, captured
+    in a CUDA graph (selection + tensor-map encoding happen at capture; replay re-issues
+    the kernels exactly)."""
 
     def __init__(self, plan, M, N, K, R, arenas, stream, side):
         import paper_2409_01075_b200 as vx
         self.R, self.M, self.N, self.K = R, M, N, K
         aA, aB, aC = arenas
-        ptrs = [(aA[i * M * K:].data_ptr(), aB[i * N * K:].data_ptr(), aC[i * M * N:].data_ptr())
-                for i in range(R)]
+        ptrs = [(aA.take(M * K), aB.take(N * K), aC.take(M * N)) for _ in range(R)]
         side.wait_stream(stream)
         with torch.cuda.stream(side):
             sp = ctypes.c_void_p(side.cuda_stream)
@@ -281,6 +298,16 @@ class PointGraph:
         stream.wait_stream(side)
 
 
+def make_arenas(pts, dev, rank, batch=1):
+    GiB = 1 << 30
+    nA = max(GiB // 2, 4 * max(batch * M * K for _, M, N, K in pts))      # elements (bf16)
+    nB = max(GiB // 2, 4 * max(batch * N * K for _, M, N, K in pts))
+    nC = max(GiB // 2, 2 * max(batch * M * N for _, M, N, K in pts))
+    return (Arena(nA, dev, "normal", 100 + rank),
+            Arena(nB, dev, "normal", 200 + rank, scale=1.0 / 64),
+            Arena(nC, dev, "empty", 0))
+
+
 def run_mine(args, rank, world, local):
     import paper_2409_01075_b200 as vx
     dev = torch.device("cuda", local)
@@ -292,16 +319,10 @@ def run_mine(args, rank, world, local):
     for _, M, N, K in pts:
         if (N, K) not in plans:
             plans[(N, K)] = vx.Plan(N, K, "bf16", "bf16", "nk", device=local)
-    Rs = [rotation(M, N, K, l2, rmax=args.rmax) for _, M, N, K in pts]
-    nA = max(R * M * K for R, (_, M, N, K) in zip(Rs, pts))
-    nB = max(R * N * K for R, (_, M, N, K) in zip(Rs, pts))
-    nC = max(R * M * N for R, (_, M, N, K) in zip(Rs, pts))
-    # operand arenas (read-only, seeded) and an output arena; point i's set j is a slice
-    aA = synth.matrix((nA,), "bf16", "normal", seed=100 + rank, device=dev)
-    aB = synth.matrix((nB,), "bf16", "normal", seed=200 + rank, scale=64 ** -1, device=dev)
-    aC = torch.empty(nC, dtype=torch.bfloat16, device=dev)
+    Rs = [R_PER_POINT] * len(pts)
+    arenas = make_arenas(pts, dev, rank)
     choices = [plans[(N, K)].select(M) for _, M, N, K in pts]
-    graphs = [PointGraph(plans[(N, K)], M, N, K, R, (aA, aB, aC), stream, side)
+    graphs = [PointGraph(plans[(N, K)], M, N, K, R, arenas, stream, side)
               for R, (_, M, N, K) in zip(Rs, pts)]
     torch.cuda.synchronize()
 
@@ -374,6 +395,7 @@ def run_mine(args, rank, world, local):
     roof["kernel"] = "vx_umma_kernel M=%d N=%d K=%d rung=%d split=%d" % (
         dom["M"], dom["N"], dom["K"], dom["rung"], dom["split"])
     roof["share_of_step"] = dom["us"] * dom["R"] / (wall_ms / args.steps) / 1e3
+    roof["launches_per_step"] = dom["R"]
     roof["peak_source"] = peaks["source"] + " burst"
 
     sharded = run_sharded(args, rank, world, local, vx, stream, side, l2)
@@ -429,12 +451,9 @@ def run_sharded(args, rank, world, local, vx, stream, side, l2):
     hi = (rank + 1) * M // world
     m = hi - lo
     p = vx.Plan(N, K, "bf16", "bf16", "nk", device=local)
-    R = rotation(m, N, K, l2)
-    dev = stream.device
-    aA = synth.matrix((R * m * K,), "bf16", "normal", seed=5000 + rank, device=dev)
-    aB = synth.matrix((R * N * K,), "bf16", "normal", seed=5001, scale=K ** -0.5, device=dev)
-    aC = torch.empty(R * m * N, dtype=torch.bfloat16, device=dev)
-    g = PointGraph(p, m, N, K, R, (aA, aB, aC), stream, side)
+    R = R_PER_POINT
+    arenas = make_arenas([("", m, N, K)], stream.device, rank)
+    g = PointGraph(p, m, N, K, R, arenas, stream, side)
     g.g.replay()
     ts = []
     barrier(world)
@@ -448,10 +467,10 @@ def run_sharded(args, rank, world, local, vx, stream, side, l2):
         ts.append(e0.elapsed_time(e1) / R)
     t = allreduce_max([statistics.median(ts)], world)[0]
     ch = p.select(m)
-    del g, aA, aB, aC
+    del g, arenas
     return {"M": M, "N": N, "K": K, "rows_per_rank": m, "ms": t,
             "tflops": flops(M, N, K) / (t * 1e-3) / 1e12, "rung": ch["rung_id"],
-            "split": ch["split"], "gather": False, "rotating_sets": R}
+            "split": ch["split"], "gather": False, "launches_per_sample": R}
 
 
 def run_e2e(args, rank, world, local, vx, plans, pts, stream):
@@ -516,8 +535,6 @@ def main():
                     help="oracle flops per sampled step (cpu_baseline / reference arm)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--points-out", default=None, help="write per-point results (json)")
-    ap.add_argument("--rmax", type=int, default=None,
-                    help="cap the rotating sets per point (ncu launch-list pass only)")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-staged e2e leg")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "mine":

@@ -7,6 +7,7 @@
 
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -18,6 +19,10 @@ namespace vx {
 
 static std::atomic<int64_t> g_launches{0};
 static unsigned long long* g_trace = nullptr;  // device buffer, 8 x u64 per CTA (debug)
+static const bool g_pdl = [] {                 // VX_PDL=0 disables programmatic launch
+    const char* e = getenv("VX_PDL");
+    return !(e && e[0] == '0');
+}();
 
 // ---- instantiated kernels (the "implemented" filter of the strategy table, R6) -----------
 bool kernel_available(int family, int bm, int bn) {
@@ -203,15 +208,24 @@ vx_status launch(const vx_plan_s* p, const vx_choice& ch, int64_t batch, int64_t
     cfg.blockDim = dim3(kThreads, 1, 1);
     cfg.dynamicSmemBytes = (size_t)smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
+    unsigned na = 0;
     if (ch.split > 1) {
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = (unsigned)ch.split;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = (unsigned)ch.split;
+        attr[na].val.clusterDim.y = 1;
+        attr[na].val.clusterDim.z = 1;
+        ++na;
     }
+    if (g_pdl) {
+        // programmatic dependent launch: this grid may start while the previous kernel on
+        // the stream drains; the kernel's griddepcontrol.wait orders all global accesses
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    cfg.attrs = na ? attr : nullptr;
+    cfg.numAttrs = na;
     // P operand (UMMA-M axis) first: A for family 0, B for the swapped family
     const CUtensorMap& mapP = swap ? mapB : mapA;
     const CUtensorMap& mapQ = swap ? mapA : mapB;
@@ -245,6 +259,7 @@ static vx_status check_args(const vx_plan_s* p, int64_t batch, int64_t M, int64_
     if (batch < 1 || M < 0 || N < 1 || K < 1) { set_error("bad sizes"); return VX_ERR_INVALID; }
     if (K != p->K) { set_error("K=%lld does not match the plan's K=%lld", (long long)K, (long long)p->K); return VX_ERR_INVALID; }
     if (p->N > 0 && N != p->N) { set_error("N=%lld does not match the plan's N=%lld", (long long)N, (long long)p->N); return VX_ERR_INVALID; }
+    if (M == 0) return VX_OK;  // empty problem: nothing is read or written
     if (!A || !B || !C) { set_error("NULL operand"); return VX_ERR_INVALID; }
     if (batch > 1 && (sA < M * K || sB < N * K || sC < M * N)) { set_error("batch strides overlap"); return VX_ERR_INVALID; }
     if (M > 0x7fffffffLL || N > 0x7fffffffLL) { set_error("M, N must fit in int32"); return VX_ERR_INVALID; }

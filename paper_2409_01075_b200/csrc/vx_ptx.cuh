@@ -149,6 +149,14 @@ __device__ __forceinline__ uint64_t sdesc_mn_sw128(uint32_t saddr, uint32_t lbo)
     return d;
 }
 
+// ---- programmatic dependent launch ---------------------------------------------------------
+// wait until the preceding grid on the stream has completed and its memory is visible
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// allow the dependent grid to be scheduled once every CTA of this grid has signalled
+__device__ __forceinline__ void grid_dep_launch() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ---- clusters / DSMEM ----------------------------------------------------------------------
 __device__ __forceinline__ uint32_t cluster_ctarank() {
     uint32_t r;

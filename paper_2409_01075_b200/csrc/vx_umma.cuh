@@ -58,7 +58,7 @@ __device__ __forceinline__ void trace_at(const UmmaParams& p, int slot) {
 
 constexpr int kEpiWarp0 = 2;
 constexpr int kThreads = 192;
-constexpr int kGroupP = 8;    // raster: 8 P-tiles x all Q-tiles per group (L2 reuse)
+constexpr int kGroupP = 16;   // raster: 16 P-tiles x all Q-tiles per group (L2 reuse)
 
 template <int BN>
 struct UmmaCfg {
@@ -172,6 +172,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
     if (threadIdx.x == 0) trace_at(p, 1);
+    // everything above (barrier init, TMEM alloc, descriptor prefetch) overlaps the previous
+    // kernel under PDL; no global memory is touched before this point
+    ptx::grid_dep_wait();
 
     // work assignment: split mode -> one tile per cluster, K range by cluster rank;
     // persistent mode -> tiles blockIdx.x, +gridDim.x, ...; whole K range
@@ -215,6 +218,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (++stage == S) { stage = 0; phase ^= 1; }
                 }
             }
+            ptx::grid_dep_launch();  // all loads issued: let the next grid start its prologue
             trace_at(p, 2);
         }
     } else if (warp == 1) {
