@@ -9,11 +9,11 @@ N in {768,2304,3072}) and LLaMA-7B (K=4096, N in {4096,11008,12288}) linear laye
 the SURVEY 8(d) d2 M sweeps (192 points), bf16 in / fp32 accumulate / bf16 out, B as an
 [N,K] weight.  One STEP = one vx_gemm call (selection + launch) per sweep point.
 
-Timing: per point, 4 back-to-back vx_gemm launches on fresh slices of >= 1 GiB operand
-arenas (cold L2: a slice is reused only after the arena wraps), captured in a CUDA graph
-(selection + tensor maps at capture); CUDA events bracket each point's graph replay on the
-launching stream; per-launch time = graph time / 4, median over the K timed steps (max
-over ranks for N > 1).  value = geomean over points of TFLOP/s (x N ranks: each rank
+Timing: one step = one CUDA graph holding, for each of the 192 points, an external event
+node and 8 back-to-back vx_gemm launches on fresh slices of >= 1 GiB operand arenas (cold
+L2: a slice is reused only after its arena wraps); selection + tensor maps run at capture.
+Per-launch time = (event[i+1] - event[i]) / 8, median over the K timed steps (max over
+ranks for N > 1).  value = geomean over points of TFLOP/s (x N ranks: each rank
 runs its own copy of the sweep -> weak scaling; no data-path collective).  The M=65536
 LLaMA FFN of configs[4] is additionally run row-sharded across the N ranks ("sharded").
 
@@ -239,15 +239,16 @@ def workload_config():
                         "sweep (SURVEY 8(d) d2), B as [N,K] weight",
             "points": len(sweep_points()), "in": "bf16", "out": "bf16", "accumulate": "fp32",
             "l2": "operands cold: every launch takes fresh slices of >= 1 GiB A/B/C arenas "
-                  "(reuse only after the arena wraps, ~8x L2); 4 launches per point per "
-                  "step, back-to-back from a CUDA graph; per-launch time = graph time / 4",
+                  "(reuse only after the arena wraps, ~8x L2); one CUDA graph per step = "
+                  "192 points x 8 back-to-back launches, external event nodes between points; "
+                  "per-launch time = point interval / 8",
             "sharded": "configs[4]: M=65536, N=11008, K=4096 row-sharded over n_gpus"}
 
 
 # ----------------------------------------------------------------------------------------
 # the product arm
 # ----------------------------------------------------------------------------------------
-R_PER_POINT = 4
+R_PER_POINT = 8
 
 
 class Arena:
@@ -272,30 +273,49 @@ class Arena:
         return p
 
 
-class PointGraph:
-    """R back-to-back vx_gemm launches of one sweep point on fresh arena slices, captured
-    in a CUDA graph (selection + tensor-map encoding happen at capture; replay re-issues
-    the kernels exactly)."""
+class SweepGraph:
+    """The whole sweep as ONE CUDA graph: for every point, an external event-record node,
+    then R back-to-back vx_gemm launches on fresh arena slices (selection + tensor-map
+    encoding happen at capture; replay re-issues exactly those kernels); a final event
+    closes the last point.  Per-launch time of point i = elapsed(ev[i], ev[i+1]) / R."""
 
-    def __init__(self, plan, M, N, K, R, arenas, stream, side):
+    def __init__(self, items, R, arenas, stream, side):
         import paper_2409_01075_b200 as vx
-        self.R, self.M, self.N, self.K = R, M, N, K
+        self.R = R
         aA, aB, aC = arenas
-        ptrs = [(aA.take(M * K), aB.take(N * K), aC.take(M * N)) for _ in range(R)]
+        work = []
+        for plan, M, N, K in items:
+            work.append((plan, M, N, K,
+                         [(aA.take(M * K), aB.take(N * K), aC.take(M * N)) for _ in range(R)]))
         side.wait_stream(stream)
         with torch.cuda.stream(side):
             sp = ctypes.c_void_p(side.cuda_stream)
-            for a, b, c in ptrs:      # kernel attributes + warm caches outside capture
+            for plan, M, N, K, ptrs in work:   # kernel attributes + warm caches, uncaptured
+                a, b, c = ptrs[0]
                 plan.gemm_ptr(1, M, N, K, a, M * K, b, N * K, c, M * N, sp)
             side.synchronize()
+            self.events = [torch.cuda.Event(enable_timing=True, external=True)
+                           for _ in range(len(work) + 1)]
             self.g = torch.cuda.CUDAGraph()
             n0 = vx.launch_count()
             with torch.cuda.graph(self.g, stream=side):
-                sp = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
-                for a, b, c in ptrs:
-                    plan.gemm_ptr(1, M, N, K, a, M * K, b, N * K, c, M * N, sp)
-            assert vx.launch_count() - n0 == R
+                cs = torch.cuda.current_stream()
+                sp = ctypes.c_void_p(cs.cuda_stream)
+                for i, (plan, M, N, K, ptrs) in enumerate(work):
+                    self.events[i].record(cs)
+                    for a, b, c in ptrs:
+                        plan.gemm_ptr(1, M, N, K, a, M * K, b, N * K, c, M * N, sp)
+                self.events[-1].record(cs)
+            self.launches = vx.launch_count() - n0
+            assert self.launches == R * len(work)
         stream.wait_stream(side)
+
+    def replay(self):
+        self.g.replay()
+
+    def per_launch_ms(self):
+        e = self.events
+        return [e[i].elapsed_time(e[i + 1]) / self.R for i in range(len(e) - 1)]
 
 
 def make_arenas(pts, dev, rank, batch=1):
@@ -322,41 +342,31 @@ def run_mine(args, rank, world, local):
     Rs = [R_PER_POINT] * len(pts)
     arenas = make_arenas(pts, dev, rank)
     choices = [plans[(N, K)].select(M) for _, M, N, K in pts]
-    graphs = [PointGraph(plans[(N, K)], M, N, K, R, arenas, stream, side)
-              for R, (_, M, N, K) in zip(Rs, pts)]
+    sweep = SweepGraph([(plans[(N, K)], M, N, K) for _, M, N, K in pts], R_PER_POINT, arenas,
+                       stream, side)
     torch.cuda.synchronize()
 
-    def one_step(record):
-        evs = []
-        for g in graphs:
-            if record:
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-            g.g.replay()
-            if record:
-                e1.record(stream)
-                evs.append((e0, e1))
-        return evs
-
     for _ in range(args.warmup):
-        one_step(False)
+        sweep.replay()
     barrier(world)
     clocks = ClockSampler(local)
     clocks.start()
     barrier(world)
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
-    t0.record(stream)
-    all_evs = [one_step(True) for _ in range(args.steps)]
-    t1.record(stream)
+    samples = []
+    wall_ms = 0.0
+    for _ in range(args.steps):
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        sweep.replay()
+        t1.record(stream)
+        t1.synchronize()
+        wall_ms += t0.elapsed_time(t1)
+        samples.append(sweep.per_launch_ms())
     barrier(world)
-    launches = args.steps * sum(Rs)
+    launches = args.steps * sweep.launches
     clk = clocks.stop()
-    wall_ms = t0.elapsed_time(t1)
-    per_pt = []
-    for j, R in enumerate(Rs):
-        per_pt.append(statistics.median(s[j][0].elapsed_time(s[j][1]) for s in all_evs) / R)
+    per_pt = [statistics.median(s_[j] for s_ in samples) for j in range(len(pts))]
     per_pt = allreduce_max(per_pt, world)
     wall_ms = allreduce_max([wall_ms], world)[0]
     peaks = load_peaks()
@@ -453,18 +463,15 @@ def run_sharded(args, rank, world, local, vx, stream, side, l2):
     p = vx.Plan(N, K, "bf16", "bf16", "nk", device=local)
     R = R_PER_POINT
     arenas = make_arenas([("", m, N, K)], stream.device, rank)
-    g = PointGraph(p, m, N, K, R, arenas, stream, side)
-    g.g.replay()
+    g = SweepGraph([(p, m, N, K)], R, arenas, stream, side)
+    g.replay()
+    torch.cuda.synchronize()
     ts = []
     barrier(world)
     for _ in range(max(3, min(args.steps, 10))):
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        g.g.replay()
-        e1.record(stream)
+        g.replay()
         torch.cuda.synchronize()
-        ts.append(e0.elapsed_time(e1) / R)
+        ts.append(g.per_launch_ms()[0])
     t = allreduce_max([statistics.median(ts)], world)[0]
     ch = p.select(m)
     del g, arenas

@@ -19,6 +19,10 @@ namespace vx {
 
 static std::atomic<int64_t> g_launches{0};
 static unsigned long long* g_trace = nullptr;  // device buffer, 8 x u64 per CTA (debug)
+static const int g_dbg = [] {                 // VX_DEBUG_FLAGS (kernel phase skips, debug only)
+    const char* e = getenv("VX_DEBUG_FLAGS");
+    return e ? atoi(e) : 0;
+}();
 static const bool g_pdl = [] {                 // VX_PDL=0 disables programmatic launch
     const char* e = getenv("VX_PDL");
     return !(e && e[0] == '0');
@@ -199,6 +203,7 @@ vx_status launch(const vx_plan_s* p, const vx_choice& ch, int64_t batch, int64_t
     prm.ldc = N;
     prm.sC = batch > 1 ? sC : M * N;
     prm.trace = g_trace;
+    prm.dbg = g_dbg;
     const int ob = p->out == VX_FP32 ? 4 : 2;
     prm.vec = (N % 8 == 0) && ((prm.sC * ob) % 16 == 0) &&
               ((reinterpret_cast<uintptr_t>(C) & 15) == 0);

@@ -45,6 +45,7 @@ struct UmmaParams {
     long long ldc;            // elements between rows of C
     long long sC;             // elements between batches of C
     unsigned long long* trace;  // optional per-CTA phase timestamps (VX_TRACE), else null
+    int dbg;                    // debug bits (VX_DEBUG_FLAGS): 1 skip push, 2 skip reduce, 4 skip C store
 };
 
 // phase trace (tracing aux subsystem): %globaltimer (ns) at fixed points, 8 slots per CTA
@@ -125,6 +126,75 @@ __device__ __forceinline__ void store4(void* C, long long idx, float4 v, int kin
         u.x = pack2(v.x, v.y, kind);
         u.y = pack2(v.z, v.w, kind);
         *reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(C) + idx) = u;
+    }
+}
+
+// ---- compact epilogue helpers ---------------------------------------------------------------
+// The epilogue runs once per tile, so its instructions are usually cold (the operand stream
+// evicts them from L2): keep this code small -- one dtype branch per chunk, rare paths out
+// of line.
+
+// 16-bit conversion of n floats (n even) into packed pairs
+template <int W>
+__device__ __forceinline__ void pack_chunk(const float* f, uint32_t* u, int kind) {
+    if (kind == 0) {
+#pragma unroll
+        for (int i = 0; i < W / 2; ++i) {
+            __nv_bfloat162 h = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+            u[i] = *reinterpret_cast<uint32_t*>(&h);
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < W / 2; ++i) {
+            __half2 h = __floats2half2_rn(f[2 * i], f[2 * i + 1]);
+            u[i] = *reinterpret_cast<uint32_t*>(&h);
+        }
+    }
+}
+
+// row-major chunk of W columns starting at column n0 of row `base` (non-swap, vector path)
+template <int W>
+__device__ __forceinline__ void store_row_chunk(char* Cb, long long base, int n0, int N,
+                                                const float* f, int kind) {
+    if (kind == 2) {
+        float* c = reinterpret_cast<float*>(Cb) + base + n0;
+#pragma unroll
+        for (int j = 0; j < W; j += 4)
+            if (n0 + j < N) *reinterpret_cast<float4*>(c + j) = make_float4(f[j], f[j + 1], f[j + 2], f[j + 3]);
+    } else {
+        uint32_t u[W / 2];
+        pack_chunk<W>(f, u, kind);
+        uint16_t* c = reinterpret_cast<uint16_t*>(Cb) + base + n0;
+#pragma unroll
+        for (int j = 0; j < W; j += 8)
+            if (n0 + j < N)
+                *reinterpret_cast<uint4*>(c + j) = make_uint4(u[j / 2], u[j / 2 + 1], u[j / 2 + 2], u[j / 2 + 3]);
+    }
+}
+
+// scalar fallback (C rows not 16-B aligned or N % 8 != 0): rare, kept out of line
+__device__ __noinline__ void store_row_scalar(char* Cb, long long base, int n0, int N, int W,
+                                              const float* f, int kind) {
+    for (int j = 0; j < W; ++j)
+        if (n0 + j < N) store1(Cb, base + n0 + j, f[j], kind);
+}
+
+// transposed chunk (swap): lane owns output column `col`, registers are rows m0..m0+W-1
+template <int W>
+__device__ __forceinline__ void store_col_chunk(char* Cb, long long ldc, int col, int m0, int M,
+                                                const float* f, int kind) {
+    if (kind == 2) {
+        float* c = reinterpret_cast<float*>(Cb) + col;
+#pragma unroll
+        for (int j = 0; j < W; ++j)
+            if (m0 + j < M) c[(long long)(m0 + j) * ldc] = f[j];
+    } else {
+        uint32_t u[W / 2];
+        pack_chunk<W>(f, u, kind);
+        uint16_t* c = reinterpret_cast<uint16_t*>(Cb) + col;
+#pragma unroll
+        for (int j = 0; j < W; ++j)
+            if (m0 + j < M) c[(long long)(m0 + j) * ldc] = (uint16_t)(u[j / 2] >> (16 * (j & 1)));
     }
 }
 
@@ -259,8 +329,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ===== epilogue warps =====
         const int quarter = warp & 3;
         const int row = quarter * 32 + lane;  // accumulator lane = row of the P tile
-        float* red = reinterpret_cast<float*>(sP);  // split mode: reuse the drained ring
-        constexpr int RS = BN + 4;                  // padded row stride (floats)
         int it = 0;
         for (int tile = tile0; tile < p.num_tiles; tile += tstep, ++it) {
             int b, tp, tq;
@@ -271,10 +339,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::tc_fence_after();
             if (it == 0 && threadIdx.x == kEpiWarp0 * 32) trace_at(p, 5);
             const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
+            if (split) break;  // split mode: the accumulator is read after the cluster barrier
             const int pr = tp * 128 + row;  // global index on the P axis
             char* Cb = reinterpret_cast<char*>(p.C) +
                        (long long)b * p.sC * (p.out_kind == 2 ? 4 : 2);
-#pragma unroll
+#pragma unroll 1
             for (int c = 0; c < (BN + 31) / 32; ++c) {
                 uint32_t v[32];
                 if (BN >= 32) ptx::tmem_ld32(taddr + c * 32, v);
@@ -282,36 +351,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::tmem_wait_ld();
                 constexpr int W = BN >= 32 ? 32 : BN;
                 const float* f = reinterpret_cast<const float*>(v);
-                if (split) {
-#pragma unroll
-                    for (int j = 0; j < W; j += 4)
-                        *reinterpret_cast<float4*>(&red[row * RS + c * 32 + j]) =
-                            make_float4(f[j], f[j + 1], f[j + 2], f[j + 3]);
+                if (p.dbg & 8) {
+                    if (f[0] == 12345.f) store1(Cb, 0, f[1], p.out_kind);
                 } else if (!SWAP) {
                     // row pr = m, columns = n
                     if (pr < p.M) {
                         const long long base = (long long)pr * p.ldc;
-#pragma unroll
-                        for (int j = 0; j < W; j += 8) {
-                            const int n = tq * BN + c * 32 + j;
-                            if (p.vec) {
-                                if (n < p.N) store8(Cb, base + n, f + j, p.out_kind);
-                            } else {
-#pragma unroll
-                                for (int e = 0; e < 8; ++e)
-                                    if (n + e < p.N) store1(Cb, base + n + e, f[j + e], p.out_kind);
-                            }
-                        }
+                        const int n0 = tq * BN + c * 32;
+                        if (p.vec) store_row_chunk<W>(Cb, base, n0, p.N, f, p.out_kind);
+                        else store_row_scalar(Cb, base, n0, p.N, W, f, p.out_kind);
                     }
-                } else {
+                } else if (pr < p.N) {
                     // row pr = n, columns = m
-                    if (pr < p.N) {
-#pragma unroll
-                        for (int j = 0; j < W; ++j) {
-                            const int m = tq * BN + c * 32 + j;
-                            if (m < p.M) store1(Cb, (long long)m * p.ldc + pr, f[j], p.out_kind);
-                        }
-                    }
+                    store_col_chunk<W>(Cb, p.ldc, pr, tq * BN + c * 32, p.M, f, p.out_kind);
                 }
             }
             ptx::tc_fence_before();
@@ -321,36 +373,69 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 
     __syncwarp();  // reconverge the single-lane roles before the .aligned cluster barriers
-    if (threadIdx.x == kEpiWarp0 * 32) trace_at(p, 6);
+    if (!split && threadIdx.x == kEpiWarp0 * 32) trace_at(p, 6);
     if (split) {
-        // deterministic in-cluster reduction: CTA `rank` owns rows [rank*128/s, +128/s) of
-        // the tile and sums the s partials in rank order 0..s-1 through DSMEM
+        // deterministic in-cluster reduce-scatter of the s K-slice partials (R7):
+        //  (1) cluster barrier: every CTA's MMAs are complete, so every SMEM ring is free;
+        //  (2) each epilogue thread reads its accumulator row from TMEM and posts it with
+        //      st.shared::cluster into slot [my rank] of the CTA owning that row (rows are
+        //      owned in blocks of 128/s);
+        //  (3) cluster barrier (release/acquire: the posted rows are visible);
+        //  (4) each CTA sums its rows over slots 0..s-1 in rank order and stores C.
+        constexpr int RS = BN + 4;                  // padded row stride (floats)
+        const int rows = 128 / p.splits;
+        const uint32_t red_addr = ptx::smem_addr(sP);
         ptx::cluster_sync();
-        if (warp >= kEpiWarp0) {
+        ptx::tc_fence_after();
+        if (warp >= kEpiWarp0 && !(p.dbg & 1)) {
+            const int quarter = warp & 3;
+            const int row = quarter * 32 + lane;
+            const int owner = row / rows;
+            const uint32_t dst = ptx::mapa(
+                red_addr + (uint32_t)(((rank * rows) + (row - owner * rows)) * RS) * 4u, owner);
+            const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16);
+#pragma unroll 1
+            for (int c = 0; c < (BN + 31) / 32; ++c) {
+                uint32_t v[32];
+                if (BN >= 32) ptx::tmem_ld32(taddr + c * 32, v);
+                else ptx::tmem_ld16(taddr + c * 32, v);
+                ptx::tmem_wait_ld();
+                constexpr int W = BN >= 32 ? 32 : BN;
+                const float* f = reinterpret_cast<const float*>(v);
+#pragma unroll
+                for (int j = 0; j < W; j += 4)
+                    ptx::st_dsmem_f4(dst + (uint32_t)(c * 32 + j) * 4u, f[j], f[j + 1], f[j + 2],
+                                     f[j + 3]);
+            }
+        }
+        ptx::cluster_sync();
+        if (threadIdx.x == kEpiWarp0 * 32) trace_at(p, 6);
+        if (warp >= kEpiWarp0 && !(p.dbg & 2)) {
             int b, tp, tq;
             decode_tile(tile0, p.tiles_p, p.tiles_q, b, tp, tq);
-            constexpr int RS = BN + 4;
-            const int rows = 128 / p.splits;
-            const int r0 = rank * rows;
             const int et = threadIdx.x - kEpiWarp0 * 32;
-            const uint32_t red_addr = ptx::smem_addr(sP);
+            const float* red = reinterpret_cast<const float*>(sP);
             char* Cb = reinterpret_cast<char*>(p.C) +
                        (long long)b * p.sC * (p.out_kind == 2 ? 4 : 2);
             const int n4 = BN / 4;
+            const int slot = rows * RS;             // floats per source-rank slot
+#pragma unroll 1
             for (int idx = et; idx < rows * n4; idx += 128) {
                 int rr, cc;
                 if (SWAP) { rr = idx % rows; cc = (idx / rows) * 4; }   // consecutive n
                 else { rr = idx / n4; cc = (idx % n4) * 4; }            // consecutive n
-                const int row = r0 + rr;
-                const uint32_t off = (uint32_t)(row * RS + cc) * 4u;
-                float4 acc4 = ptx::ld_dsmem_f4(ptx::mapa(red_addr + off, 0));
+                const float* src = red + rr * RS + cc;
+                float4 acc4 = *reinterpret_cast<const float4*>(src);
+#pragma unroll 1
                 for (int j = 1; j < p.splits; ++j) {
-                    float4 t = ptx::ld_dsmem_f4(ptx::mapa(red_addr + off, j));
+                    const float4 t = *reinterpret_cast<const float4*>(src + j * slot);
                     acc4.x += t.x; acc4.y += t.y; acc4.z += t.z; acc4.w += t.w;
                 }
-                const int pr = tp * 128 + row;
+                const int pr = tp * 128 + rank * rows + rr;
                 const int q0 = tq * BN + cc;
-                if (!SWAP) {
+                if (p.dbg & 4) {
+                    if (acc4.x == 12345.f) store1(Cb, 0, acc4.y, p.out_kind);
+                } else if (!SWAP) {
                     if (pr < p.M) {
                         if (p.vec) {
                             if (q0 < p.N) store4(Cb, (long long)pr * p.ldc + q0, acc4, p.out_kind);
@@ -369,12 +454,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
         }
-        ptx::cluster_sync();
     }
 
+    if (threadIdx.x == kEpiWarp0 * 32) trace_at(p, 7);
     ptx::tc_fence_before();
     __syncthreads();
-    if (threadIdx.x == 0) trace_at(p, 7);
     if (warp == 1) {
         __syncwarp();
         ptx::tc_fence_after();

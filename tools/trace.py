@@ -6,7 +6,7 @@ import numpy as np, torch
 import paper_2409_01075_b200 as vx
 import synth
 
-PH = ["entry", "setup", "prod_done", "first_full", "mma_done", "acc_ready", "epi_done", "end"]
+PH = ["entry", "setup", "prod_done", "first_full", "mma_done", "acc_ready", "epi/sync2", "reduced"]
 
 def main():
     a = [x for x in sys.argv[1:] if not x.startswith("--")]
