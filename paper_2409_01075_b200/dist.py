@@ -1,0 +1,92 @@
+"""Multi-GPU M-row sharding of the dynamic-M GEMM.
+
+Rows of C depend only on the same rows of A (C = A x B), so the problem
+partitions by M rows with B replicated: every rank runs its own vx_gemm on its row block
+and no reduction is needed.  A gathered C is produced only when asked for, with ONE
+collective: all_gather_into_tensor over NCCL (NVLink 5 / NVSwitch on B200).  Uneven M is
+handled by padding every shard to the largest shard in the gather buffer and trimming.
+
+Everything here is host-side plumbing; the GEMM itself is the library call.  The
+collective goes through a torch.distributed process group, so the same code runs on the
+"gloo" backend with CPU tensors (tests/test_dist.py) and on "nccl" with CUDA tensors.
+"""
+from __future__ import annotations
+
+from typing import Callable
+
+import torch
+
+
+def row_shard(M: int, world: int, rank: int) -> tuple[int, int]:
+    """[lo, hi) rows of rank `rank`: contiguous, disjoint, covering [0, M), sizes differ by
+    at most one (the first M % world ranks get one extra row)."""
+    if world < 1 or not 0 <= rank < world or M < 0:
+        raise ValueError("bad shard arguments")
+    base, extra = divmod(M, world)
+    lo = rank * base + min(rank, extra)
+    hi = lo + base + (1 if rank < extra else 0)
+    return lo, hi
+
+
+def shard_sizes(M: int, world: int) -> list[int]:
+    return [row_shard(M, world, r)[1] - row_shard(M, world, r)[0] for r in range(world)]
+
+
+def gather_rows(c_local: torch.Tensor, M: int, group=None) -> torch.Tensor:
+    """All-gather row shards (each rank's [m_r, N] block, m_r from row_shard) into the full
+    [M, N] C on every rank.  One all_gather_into_tensor of max-size padded shards."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    sizes = shard_sizes(M, world)
+    if c_local.shape[0] != sizes[rank]:
+        raise ValueError("local shard has %d rows, expected %d" % (c_local.shape[0], sizes[rank]))
+    mmax = max(sizes) if sizes else 0
+    N = c_local.shape[1]
+    send = c_local
+    if c_local.shape[0] != mmax:
+        send = torch.zeros((mmax, N), dtype=c_local.dtype, device=c_local.device)
+        send[: c_local.shape[0]] = c_local
+    recv = torch.empty((world * mmax, N), dtype=c_local.dtype, device=c_local.device)
+    dist.all_gather_into_tensor(recv, send.contiguous(), group=group)
+    if all(s == mmax for s in sizes):
+        return recv
+    parts = [recv[r * mmax: r * mmax + sizes[r]] for r in range(world)]
+    return torch.cat(parts, 0)
+
+
+class ShardedGemm:
+    """C = A x B with A row-sharded over the ranks of `group` and B replicated.
+
+    local_gemm(A_rows, B) -> C_rows runs on this rank's device; by default it is the
+    library's Plan.gemm.  forward() takes either the full A (each rank slices its rows) or
+    this rank's shard, and returns this rank's C rows, or the gathered C if gather=True.
+    """
+
+    def __init__(self, N: int, K: int, group=None, local_gemm: Callable | None = None,
+                 in_dtype: str = "bf16", out_dtype: str = "bf16", b_layout: str = "nk",
+                 device: int | None = None):
+        import torch.distributed as dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.N, self.K = N, K
+        if local_gemm is None:
+            from . import Plan
+            plan = Plan(N, K, in_dtype, out_dtype, b_layout,
+                        device=device if device is not None else torch.cuda.current_device())
+            local_gemm = lambda a, b: plan.gemm(a, b)  # noqa: E731
+        self.local_gemm = local_gemm
+
+    def forward(self, A: torch.Tensor, B: torch.Tensor, M: int | None = None,
+                gather: bool = False) -> torch.Tensor:
+        if M is None:            # full A given: take this rank's rows
+            M = A.shape[0]
+            lo, hi = row_shard(M, self.world, self.rank)
+            A = A[lo:hi].contiguous()
+        else:
+            lo, hi = row_shard(M, self.world, self.rank)
+            if A.shape[0] != hi - lo:
+                raise ValueError("A shard has %d rows, expected %d" % (A.shape[0], hi - lo))
+        c = self.local_gemm(A, B)
+        return gather_rows(c, M, self.group) if gather else c

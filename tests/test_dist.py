@@ -1,0 +1,84 @@
+"""Multi-process host logic of the M-row-sharded GEMM on CPU (gloo, world size 2 and 3).
+
+The local GEMM is injected (the fp64 oracle -- test infrastructure), so these tests cover
+exactly the sharding / gather plumbing of paper_2409_01075_b200/dist.py that the NCCL run
+uses on B200s.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2409_01075_b200.dist import ShardedGemm, gather_rows, row_shard, shard_sizes
+
+
+def test_row_shard_partition_properties():
+    for M in (0, 1, 7, 128, 1000, 65536, 65537):
+        for world in (1, 2, 3, 4, 8):
+            spans = [row_shard(M, world, r) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == M
+            for (a, b), (c, d) in zip(spans, spans[1:]):
+                assert b == c and a <= b
+            sizes = shard_sizes(M, world)
+            assert sum(sizes) == M and max(sizes) - min(sizes) <= 1
+    assert row_shard(65536, 8, 3) == (3 * 8192, 4 * 8192)
+    with pytest.raises(ValueError):
+        row_shard(10, 2, 2)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, M, N, K, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        import synth
+        A, B = synth.gemm_inputs(M, N, K, "fp32", "nk", kind="int", seed=42)   # same on all ranks
+
+        def local(a, b):
+            return torch.from_numpy(oracle.gemm(a, b, "nk")).float()
+
+        sg = ShardedGemm(N, K, local_gemm=local)
+        c_rows = sg.forward(A, B)                        # this rank's rows only
+        lo, hi = row_shard(M, world, rank)
+        ok_rows = c_rows.shape == (hi - lo, N)
+        C = sg.forward(A, B, gather=True)                # gathered on every rank
+        lo_ = torch.tensor([lo], dtype=torch.int64)
+        C2 = gather_rows(c_rows, M)                      # the gather alone
+        q.put((rank, ok_rows, C.numpy(), C2.numpy(), int(lo_)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,M", [(2, 37), (2, 64), (3, 100), (2, 1)])
+def test_sharded_gather_equals_full_gemm(world, M):
+    import oracle
+    import synth
+    N, K = 24, 40
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, M, N, K, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    A, B = synth.gemm_inputs(M, N, K, "fp32", "nk", kind="int", seed=42)
+    want = oracle.gemm(A, B, "nk")
+    for rank, ok_rows, C, C2, lo in res:
+        assert ok_rows
+        assert np.array_equal(C, want) and np.array_equal(C2, want)

@@ -1,0 +1,155 @@
+"""Empirical tier of the hybrid analyzer: profile every rung of the
+ladder once on a FIXED, GENERIC grid of calibration shapes (tile multiples and tails; not
+the benchmark workload, no sample list), then fit the rung constants of the analytical
+model to the measurements.
+
+    measure (GPU):  python tools/calibrate.py measure --out gpurun_out/calib_raw.json
+    fit (CPU):      python tools/calibrate.py fit gpurun_out/calib_raw.json
+
+The fit re-implements the DESIGN.md 3.3 formula in float form (no ceilings) -- it is a
+tool, independent of both the library and the oracle; its output is written by hand into
+csrc/vx_calib.cpp and oracle/calib_b200.json, whose equality is tested.
+"""
+import argparse
+import ctypes
+import json
+import math
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+CAL_M = (1, 8, 32, 64, 128, 200, 512, 1024, 2048, 4096, 8192)
+CAL_NK = ((1024, 1024), (4096, 1024), (2048, 4096), (8192, 4096), (6144, 2048))
+CLOCK_GHZ = 1.965   # cycles of the model are SM cycles at the max clock
+
+
+def measure(args):
+    import torch
+    import paper_2409_01075_b200 as vx
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    from sweep import time_graph
+    dev = torch.device("cuda", 0)
+    stream = torch.cuda.current_stream(dev)
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    out = {"desc": vx.device_probe(0).to_json(), "clock_ghz": CLOCK_GHZ, "samples": []}
+    for N, K in CAL_NK:
+        p = vx.Plan(N, K, "bf16", "bf16", "nk")
+        rungs = p.dump()["rungs"]
+        for M in CAL_M:
+            for r in rungs:
+                for s in r["splits"]:
+                    t = time_graph(p, 1, M, N, K, r["rung_id"], s, dev, stream, l2, 3, "nk")
+                    out["samples"].append({"M": M, "N": N, "K": K, "rung": r["rung_id"],
+                                           "family": r["family"], "bm": r["bm"], "bn": r["bn"],
+                                           "stages": r["stages"], "split": s, "us": t})
+            print("N=%d K=%d M=%d done" % (N, K, M), flush=True)
+    json.dump(out, open(args.out, "w"))
+
+
+# ---- float model (DESIGN.md 3.3 without ceilings) ------------------------------------------
+def model_us(sm, th, desc, g):
+    """th: per-rung dict mac,l2s,epi,fixed (bytes or MACs per cycle); g: hbm,dsm,fixed_cluster."""
+    M, N, K, s = sm["M"], sm["N"], sm["K"], sm["split"]
+    bm, bn, bk = sm["bm"], sm["bn"], 64
+    swap = sm["family"] == 1
+    mt, nt = (N, M) if swap else (M, N)
+    tm, tn = -(-mt // bm), -(-nt // bn)
+    tiles = tm * tn
+    kb = -(-K // bk)
+    trips = kb // s
+    W = tiles * s
+    slots = desc["max_active_clusters"][str(s)] * s
+    F = -(-W // slots)
+    c = bm * bn * bk / th["mac"]
+    l = max((bm + bn) * bk * 2 / th["l2s"], 2 * K * (mt + nt) / (F * trips * g["hbm"]))
+    st = max(bm * bn * 2 / (s * th["epi"]), 2 * M * N / (F * g["hbm"]))
+    if s > 1:
+        st += (s - 1) * bm * bn * 4 / (s * g["dsm"])
+    T = l + (trips - 1) * max(l, c) + c + st
+    if s == 1:
+        tmain = T - st
+        cyc = tmain + (F - 1) * max(tmain, st) + st + th["fixed"]
+    else:
+        cyc = F * T + th["fixed"] + g["fixed_cluster"]
+    return cyc / (CLOCK_GHZ * 1e3)
+
+
+def fit(args):
+    import numpy as np
+    from scipy.optimize import minimize
+    raw = json.load(open(args.raw))
+    desc = raw["desc"]
+    S = raw["samples"]
+    keys = sorted({("umma_swap" if x["family"] == 1 else "umma", x["bm"], x["bn"]) for x in S})
+    names = ["%s_%dx%d" % k for k in keys]
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    hbm = peaks["hbm_gbs"] / CLOCK_GHZ
+    # parameter vector: log of (mac, l2s, epi, fixed) per rung + log(dsm, fixed_cluster)
+    x0 = []
+    for k in keys:
+        x0 += [math.log(4096 if k[2] >= 128 else 2048), math.log(96), math.log(64), math.log(3000)]
+    x0 += [math.log(20), math.log(1500)]
+
+    def unpack(x):
+        th = {}
+        for i, n in enumerate(names):
+            th[n] = dict(mac=math.exp(x[4 * i]), l2s=math.exp(x[4 * i + 1]),
+                         epi=math.exp(x[4 * i + 2]), fixed=math.exp(x[4 * i + 3]))
+        g = dict(hbm=hbm, dsm=math.exp(x[-2]), fixed_cluster=math.exp(x[-1]))
+        return th, g
+
+    def key_of(x):
+        return "%s_%dx%d" % ("umma_swap" if x["family"] == 1 else "umma", x["bm"], x["bn"])
+
+    def loss(x):
+        th, g = unpack(x)
+        e = 0.0
+        for sm in S:
+            pred = model_us(sm, th[key_of(sm)], desc, g)
+            e += (math.log(pred) - math.log(sm["us"])) ** 2
+        return e / len(S)
+
+    res = minimize(loss, np.array(x0), method="Powell", options={"maxiter": 20000, "xtol": 1e-3})
+    th, g = unpack(res.x)
+    print("rms log error %.3f" % math.sqrt(res.fun))
+    # regret of the fitted model on the calibration grid
+    groups = {}
+    for sm in S:
+        groups.setdefault((sm["M"], sm["N"], sm["K"]), []).append(sm)
+    regrets = []
+    for k, v in groups.items():
+        best = min(x["us"] for x in v)
+        pick = min(v, key=lambda x: model_us(x, th[key_of(x)], desc, g))
+        regrets.append(best / pick["us"])
+    print("calibration-grid regret geomean %.4f worst %.4f" % (
+        math.exp(sum(math.log(r) for r in regrets) / len(regrets)), min(regrets)))
+    out = {"hbm_milli": int(round(hbm * 1000)), "dsm_milli": int(round(g["dsm"] * 1000)),
+           "fixed_cluster": int(round(g["fixed_cluster"])), "rungs": {}}
+    for n in names:
+        t = th[n]
+        out["rungs"][n] = {"mac_milli": int(round(t["mac"] * 1000)),
+                           "l2s_milli": int(round(t["l2s"] * 1000)),
+                           "epi_milli": int(round(t["epi"] * 1000)),
+                           "fixed": int(round(t["fixed"]))}
+    print(json.dumps(out, indent=1))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    sub = ap.add_subparsers(dest="cmd")
+    m = sub.add_parser("measure")
+    m.add_argument("--out", default="gpurun_out/calib_raw.json")
+    f = sub.add_parser("fit")
+    f.add_argument("raw")
+    args = ap.parse_args()
+    if args.cmd == "measure":
+        measure(args)
+    else:
+        fit(args)
+
+
+if __name__ == "__main__":
+    main()
