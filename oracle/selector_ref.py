@@ -129,7 +129,8 @@ UMMA_K = 16                                      # kind::f16: K = 32 bytes / 2-b
 BK_TC = 64                                       # one 128-B swizzle row of 2-byte elements
 SPLITS = (1, 2, 4, 8)                            # R7
 MAX_STAGES = 16                                  # R5
-SMEM_RESERVE = 1024                              # barriers + 1024-B alignment slack
+SMEM_RESERVE = 2048                              # barriers + 1024-B alignment slack
+EPI_STAGING = 32768                              # epilogue: 4 warps x 2 x 4 KB TMA-store tiles
 CLUSTER_MAX = 8                                  # portable cluster size
 
 # kernels that exist in the library (the "implemented" filter, R6):
@@ -181,11 +182,11 @@ def build_table(K: int, in_dtype: str, out_dtype: str, desc: dict) -> dict:
             cg = 2 if am == 256 else 1
             bm_cta, bn_cta = am // cg, an // cg
             stage_bytes = (bm_cta + bn_cta) * BK_TC * in_b
-            s_fit = (cap - SMEM_RESERVE) // stage_bytes
+            s_fit = (cap - SMEM_RESERVE - EPI_STAGING) // stage_bytes
             S = min(MAX_STAGES, s_fit)
             if S < 2:
                 continue
-            foot = S * stage_bytes + SMEM_RESERVE
+            foot = S * stage_bytes + SMEM_RESERVE + EPI_STAGING
             if foot * 8 < cap:            # utilisation window [1/8, 1] (R3)
                 continue
             l2_init.append((am, an, BK_TC, S, st))

@@ -36,7 +36,7 @@ bool kernel_available(int family, int bm, int bn) {
     return false;
 }
 
-using UmmaFn = void (*)(const CUtensorMap, const CUtensorMap, const UmmaParams);
+using UmmaFn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const UmmaParams);
 
 template <int BN, bool SWAP>
 static UmmaFn pick_mn(bool b_mn) {
@@ -76,7 +76,7 @@ static SimtFn simt_fn(int bm, int bn, int* threads) {
 }
 
 static int64_t umma_smem_bytes(int bn, int stages) {
-    return (int64_t)stages * (128 + bn) * kBkTc * 2 + kSmemReserve;
+    return (int64_t)stages * (128 + bn) * kBkTc * 2 + kSmemReserve + kEpiStaging;
 }
 
 static vx_status cuda_fail(cudaError_t e, const char* what) {
@@ -124,16 +124,20 @@ static EncodeTiledFn encode_fn() {
 // dims {inner, rows, batch}; box {64, box_rows, 1}; 128-B swizzle; OOB -> zeros.
 static vx_status make_map(CUtensorMap* map, const void* base, vx_dtype dt, int64_t inner,
                           int64_t rows, int64_t batch, int64_t ld, int64_t bstride,
-                          int box_inner, int box_rows) {
+                          int box_inner, int box_rows, bool swizzle = true) {
     EncodeTiledFn enc = encode_fn();
     if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return VX_ERR_CUDA; }
+    const int eb = dt == VX_FP32 ? 4 : 2;
     cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)rows, (cuuint64_t)batch};
-    cuuint64_t strides[2] = {(cuuint64_t)ld * 2, (cuuint64_t)bstride * 2};
+    cuuint64_t strides[2] = {(cuuint64_t)ld * eb, (cuuint64_t)bstride * eb};
     cuuint32_t box[3] = {(cuuint32_t)box_inner, (cuuint32_t)box_rows, 1};
     cuuint32_t estr[3] = {1, 1, 1};
-    CUresult r = enc(map, dt == VX_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
-                     3, const_cast<void*>(base), dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+    const CUtensorMapDataType ty = dt == VX_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                 : dt == VX_FP16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                                 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    CUresult r = enc(map, ty, 3, const_cast<void*>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
         set_error("cuTensorMapEncodeTiled failed (%d): inner=%lld rows=%lld batch=%lld ld=%lld",
@@ -207,6 +211,15 @@ vx_status launch(const vx_plan_s* p, const vx_choice& ch, int64_t batch, int64_t
     const int ob = p->out == VX_FP32 ? 4 : 2;
     prm.vec = (N % 8 == 0) && ((prm.sC * ob) % 16 == 0) &&
               ((reinterpret_cast<uintptr_t>(C) & 15) == 0);
+    // C map for the TMA-store epilogue: non-swap boxes are 128-B rows x 32 rows (swizzled),
+    // swap boxes are 32 n x min(32, BN) m (plain)
+    CUtensorMap mapC;
+    memset(&mapC, 0, sizeof(mapC));
+    if (prm.vec) {
+        if (!swap) s = make_map(&mapC, C, p->out, N, M, batch, N, prm.sC, 128 / ob, 32, true);
+        else s = make_map(&mapC, C, p->out, N, M, batch, N, prm.sC, 32, r.bn < 32 ? r.bn : 32, false);
+        if (s != VX_OK) return s;
+    }
 
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)ch.grid, 1, 1);
@@ -234,7 +247,7 @@ vx_status launch(const vx_plan_s* p, const vx_choice& ch, int64_t batch, int64_t
     // P operand (UMMA-M axis) first: A for family 0, B for the swapped family
     const CUtensorMap& mapP = swap ? mapB : mapA;
     const CUtensorMap& mapQ = swap ? mapA : mapB;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, fn, mapP, mapQ, prm);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, fn, mapP, mapQ, mapC, prm);
     if (e != cudaSuccess) return cuda_fail(e, "tcgen05 launch");
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return VX_OK;

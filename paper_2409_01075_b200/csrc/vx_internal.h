@@ -19,6 +19,7 @@ constexpr int kBkTc = 64;          // one 128-B swizzle row of 2-byte elements
 constexpr int kUmmaK = 16;         // kind::f16 instruction K
 constexpr int kMaxStages = 16;     // R5
 constexpr int kSmemReserve = 2048; // barriers + 1024-B alignment slack
+constexpr int kEpiStaging = 32768; // epilogue: 4 warps x 2 x 4 KB TMA-store staging tiles
 constexpr int kClusterMax = 8;     // portable cluster size
 constexpr int kSimtBk = 16;
 

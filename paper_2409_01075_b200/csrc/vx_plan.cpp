@@ -117,10 +117,10 @@ static vx_status build_rungs(vx_plan_s* p) {
         for (const L1& a : l1) {
             int cg = a.am == 256 ? 2 : 1;
             int64_t stage = (int64_t)(a.am / cg + a.an / cg) * kBkTc * in_b;
-            int64_t fit = (d.smem_optin - kSmemReserve) / stage;
+            int64_t fit = (d.smem_optin - kSmemReserve - kEpiStaging) / stage;
             int S = (int)std::min<int64_t>(kMaxStages, fit);
             if (S < 2) continue;
-            int64_t foot = S * stage + kSmemReserve;
+            int64_t foot = S * stage + kSmemReserve + kEpiStaging;
             if (foot * 8 < d.smem_optin) continue;
             l2i.push_back({a.am, a.an, kBkTc, S, a.st});
         }

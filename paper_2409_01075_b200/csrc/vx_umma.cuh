@@ -202,7 +202,7 @@ __device__ __forceinline__ void store_col_chunk(char* Cb, long long ldc, int col
 template <int BN, bool SWAP, bool P_MN, bool Q_MN>
 __global__ void __launch_bounds__(kThreads, 1)
     vx_umma_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmQ,
-                   const UmmaParams p) {
+                   const __grid_constant__ CUtensorMap tmC, const UmmaParams p) {
     using Cfg = UmmaCfg<BN>;
     constexpr int kP = Cfg::kPBytes, kQ = Cfg::kQBytes;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -222,10 +222,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tile_off = ((raw_addr + 512 + 1023) & ~1023u) - raw_addr;
     uint8_t* sP = smem_raw + tile_off;
     uint8_t* sQ = sP + S * kP;
+    uint8_t* sE = sQ + S * kQ;  // epilogue staging: 4 warps x 2 x 4 KB (TMA-store tiles)
 
     if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&tmP);
         ptx::prefetch_tmap(&tmQ);
+        if (p.vec) ptx::prefetch_tmap(&tmC);
         for (int i = 0; i < S; ++i) {
             ptx::mbar_init(&full[i], 1);
             ptx::mbar_init(&empty[i], 1);
@@ -329,6 +331,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ===== epilogue warps =====
         const int quarter = warp & 3;
         const int row = quarter * 32 + lane;  // accumulator lane = row of the P tile
+        const uint32_t wstage = ptx::smem_addr(sE) + (uint32_t)(warp - kEpiWarp0) * 8192u;
+        int sc = 0;                            // staging buffers used so far (alternating)
         int it = 0;
         for (int tile = tile0; tile < p.num_tiles; tile += tstep, ++it) {
             int b, tp, tq;
@@ -340,6 +344,91 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (it == 0 && threadIdx.x == kEpiWarp0 * 32) trace_at(p, 5);
             const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
             if (split) break;  // split mode: the accumulator is read after the cluster barrier
+            if (p.vec && !(p.dbg & 8)) {
+                // TMEM -> registers -> swizzled SMEM staging -> TMA bulk store (full lines,
+                // asynchronous, M/N tails clipped by the tensor map)
+                const int ob = p.out_kind == 2 ? 4 : 2;
+                if (!SWAP) {
+                    const int CW = 128 / ob;                  // columns per 128-B row
+#pragma unroll 1
+                    for (int k = 0; k < BN / CW; ++k, ++sc) {
+                        const uint32_t buf = wstage + (uint32_t)(sc & 1) * 4096u;
+                        if (sc >= 2) {
+                            if (lane == 0) ptx::bulk_wait_read<1>();
+                            __syncwarp();
+                        }
+                        const uint32_t rowa = buf + (uint32_t)lane * 128u;
+#pragma unroll 1
+                        for (int h = 0; h < CW / 32; ++h) {   // 32 TMEM columns at a time
+                            uint32_t v[32];
+                            ptx::tmem_ld32(taddr + k * CW + h * 32, v);
+                            ptx::tmem_wait_ld();
+                            const float* f = reinterpret_cast<const float*>(v);
+                            if (ob == 4) {                    // 8 x 16-B chunks of 4 floats
+#pragma unroll
+                                for (int j = 0; j < 8; ++j)
+                                    ptx::st_shared_v4(rowa + (((uint32_t)(j ^ (lane & 7))) << 4),
+                                                      v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                            } else {                          // 4 x 16-B chunks of 8 halves
+                                uint32_t u[16];
+                                pack_chunk<32>(f, u, p.out_kind);
+#pragma unroll
+                                for (int j = 0; j < 4; ++j) {
+                                    const uint32_t jj = (uint32_t)(h * 4 + j);
+                                    ptx::st_shared_v4(rowa + ((jj ^ (uint32_t)(lane & 7)) << 4),
+                                                      u[4 * j], u[4 * j + 1], u[4 * j + 2], u[4 * j + 3]);
+                                }
+                            }
+                        }
+                        ptx::fence_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            ptx::tma_store_3d(&tmC, sE + (buf - ptx::smem_addr(sE)),
+                                              tq * BN + k * CW, tp * 128 + quarter * 32, b);
+                            ptx::bulk_commit();
+                        }
+                    }
+                } else {
+                    constexpr int W = BN >= 32 ? 32 : BN;     // m values per chunk
+#pragma unroll 1
+                    for (int c = 0; c < BN / W; ++c, ++sc) {
+                        const uint32_t buf = wstage + (uint32_t)(sc & 1) * 4096u;
+                        if (sc >= 2) {
+                            if (lane == 0) ptx::bulk_wait_read<1>();
+                            __syncwarp();
+                        }
+                        uint32_t v[32];
+                        if (BN >= 32) ptx::tmem_ld32(taddr + c * 32, v);
+                        else ptx::tmem_ld16(taddr + c * 32, v);
+                        ptx::tmem_wait_ld();
+                        const float* f = reinterpret_cast<const float*>(v);
+                        // staging tile [W m-rows][32 n] (row pitch 32*ob bytes), lane = n
+                        if (ob == 4) {
+#pragma unroll
+                            for (int j = 0; j < W; ++j)
+                                ptx::st_shared_u32(buf + (uint32_t)(j * 32 + lane) * 4u, v[j]);
+                        } else {
+                            uint32_t u[W / 2];
+                            pack_chunk<W>(f, u, p.out_kind);
+#pragma unroll
+                            for (int j = 0; j < W; ++j)
+                                ptx::st_shared_u16(buf + (uint32_t)(j * 32 + lane) * 2u,
+                                                   (uint16_t)(u[j / 2] >> (16 * (j & 1))));
+                        }
+                        ptx::fence_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            ptx::tma_store_3d(&tmC, sE + (buf - ptx::smem_addr(sE)),
+                                              tp * 128 + quarter * 32, tq * BN + c * W, b);
+                            ptx::bulk_commit();
+                        }
+                    }
+                }
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+                continue;
+            }
             const int pr = tp * 128 + row;  // global index on the P axis
             char* Cb = reinterpret_cast<char*>(p.C) +
                        (long long)b * p.sC * (p.out_kind == 2 ? 4 : 2);
@@ -370,6 +459,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
         }
+        if (lane == 0) ptx::bulk_wait<0>();   // TMA stores complete before the CTA retires
     }
 
     __syncwarp();  // reconverge the single-lane roles before the .aligned cluster barriers

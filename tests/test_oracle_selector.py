@@ -94,7 +94,7 @@ def test_table_invariants(K):
         assert r["bm"] % r["um"] == 0 and r["bn"] % r["un"] == 0 and r["bk"] % S.UMMA_K == 0
         assert S.isa_compatible_f16((r["um"], r["un"], S.UMMA_K))
         # resources: SMEM stages fit, TMEM accumulators fit
-        foot = r["stages"] * (r["bm"] + r["bn"]) * r["bk"] * 2 + S.SMEM_RESERVE
+        foot = r["stages"] * (r["bm"] + r["bn"]) * r["bk"] * 2 + S.SMEM_RESERVE + S.EPI_STAGING
         assert foot <= DESC["smem_optin"] and r["stages"] >= 2
         assert r["acc_stages"] * r["bn"] <= DESC["tmem_cols"]
         # split-K slices are whole k-blocks
