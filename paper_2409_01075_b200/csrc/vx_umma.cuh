@@ -58,7 +58,9 @@ __device__ __forceinline__ void trace_at(const UmmaParams& p, int slot) {
 }
 
 constexpr int kEpiWarp0 = 2;
-constexpr int kThreads = 192;
+constexpr int kEpiWarps = 8;   // two warps per TMEM lane quarter, splitting the column chunks
+constexpr int kEpiThreads = kEpiWarps * 32;
+constexpr int kThreads = kEpiWarp0 * 32 + kEpiThreads;
 constexpr int kGroupP = 16;   // raster: 16 P-tiles x all Q-tiles per group (L2 reuse)
 
 template <int BN>
@@ -234,7 +236,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(&tfull[i], 1);
-            ptx::mbar_init(&tempty[i], 4);
+            ptx::mbar_init(&tempty[i], kEpiWarps);
         }
         ptx::fence_mbar_init();
     }
@@ -329,10 +331,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else {
         // ===== epilogue warps =====
+        // warp w reads TMEM lanes 32*(w%4)..+31 (its quarter of the tile rows); the two
+        // warps of a quarter (group g = 0, 1) take alternate column chunks
         const int quarter = warp & 3;
+        const int grp = (warp - kEpiWarp0) >> 2;
         const int row = quarter * 32 + lane;  // accumulator lane = row of the P tile
-        const uint32_t wstage = ptx::smem_addr(sE) + (uint32_t)(warp - kEpiWarp0) * 8192u;
-        int sc = 0;                            // staging buffers used so far (alternating)
+        const uint32_t wbuf = ptx::smem_addr(sE) + (uint32_t)(warp - kEpiWarp0) * 4096u;
+        bool pending = false;                  // a TMA store still reads this warp's buffer
         int it = 0;
         for (int tile = tile0; tile < p.num_tiles; tile += tstep, ++it) {
             int b, tp, tq;
@@ -350,51 +355,49 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int ob = p.out_kind == 2 ? 4 : 2;
                 if (!SWAP) {
                     const int CW = 128 / ob;                  // columns per 128-B row
+                    const uint32_t rowa = wbuf + (uint32_t)lane * 128u;
 #pragma unroll 1
-                    for (int k = 0; k < BN / CW; ++k, ++sc) {
-                        const uint32_t buf = wstage + (uint32_t)(sc & 1) * 4096u;
-                        if (sc >= 2) {
-                            if (lane == 0) ptx::bulk_wait_read<1>();
+                    for (int k = grp; k < BN / CW; k += 2) {
+                        if (pending) {
+                            if (lane == 0) ptx::bulk_wait_read<0>();
                             __syncwarp();
                         }
-                        const uint32_t rowa = buf + (uint32_t)lane * 128u;
-#pragma unroll 1
-                        for (int h = 0; h < CW / 32; ++h) {   // 32 TMEM columns at a time
+                        if (ob == 4) {                        // 32 fp32 = 8 x 16-B chunks
                             uint32_t v[32];
-                            ptx::tmem_ld32(taddr + k * CW + h * 32, v);
+                            ptx::tmem_ld32(taddr + k * CW, v);
                             ptx::tmem_wait_ld();
-                            const float* f = reinterpret_cast<const float*>(v);
-                            if (ob == 4) {                    // 8 x 16-B chunks of 4 floats
 #pragma unroll
-                                for (int j = 0; j < 8; ++j)
-                                    ptx::st_shared_v4(rowa + (((uint32_t)(j ^ (lane & 7))) << 4),
-                                                      v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-                            } else {                          // 4 x 16-B chunks of 8 halves
-                                uint32_t u[16];
-                                pack_chunk<32>(f, u, p.out_kind);
+                            for (int j = 0; j < 8; ++j)
+                                ptx::st_shared_v4(rowa + (((uint32_t)(j ^ (lane & 7))) << 4),
+                                                  v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                        } else {                              // 64 halves = 8 x 16-B chunks
+                            uint32_t v[64];
+                            ptx::tmem_ld32(taddr + k * CW, *reinterpret_cast<uint32_t(*)[32]>(v));
+                            ptx::tmem_ld32(taddr + k * CW + 32,
+                                           *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+                            ptx::tmem_wait_ld();
+                            uint32_t u[32];
+                            pack_chunk<64>(reinterpret_cast<const float*>(v), u, p.out_kind);
 #pragma unroll
-                                for (int j = 0; j < 4; ++j) {
-                                    const uint32_t jj = (uint32_t)(h * 4 + j);
-                                    ptx::st_shared_v4(rowa + ((jj ^ (uint32_t)(lane & 7)) << 4),
-                                                      u[4 * j], u[4 * j + 1], u[4 * j + 2], u[4 * j + 3]);
-                                }
-                            }
+                            for (int j = 0; j < 8; ++j)
+                                ptx::st_shared_v4(rowa + (((uint32_t)(j ^ (lane & 7))) << 4),
+                                                  u[4 * j], u[4 * j + 1], u[4 * j + 2], u[4 * j + 3]);
                         }
                         ptx::fence_async_smem();
                         __syncwarp();
                         if (lane == 0) {
-                            ptx::tma_store_3d(&tmC, sE + (buf - ptx::smem_addr(sE)),
+                            ptx::tma_store_3d(&tmC, sE + (wbuf - ptx::smem_addr(sE)),
                                               tq * BN + k * CW, tp * 128 + quarter * 32, b);
                             ptx::bulk_commit();
                         }
+                        pending = true;
                     }
                 } else {
                     constexpr int W = BN >= 32 ? 32 : BN;     // m values per chunk
 #pragma unroll 1
-                    for (int c = 0; c < BN / W; ++c, ++sc) {
-                        const uint32_t buf = wstage + (uint32_t)(sc & 1) * 4096u;
-                        if (sc >= 2) {
-                            if (lane == 0) ptx::bulk_wait_read<1>();
+                    for (int c = grp; c < BN / W; c += 2) {
+                        if (pending) {
+                            if (lane == 0) ptx::bulk_wait_read<0>();
                             __syncwarp();
                         }
                         uint32_t v[32];
@@ -406,22 +409,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                         if (ob == 4) {
 #pragma unroll
                             for (int j = 0; j < W; ++j)
-                                ptx::st_shared_u32(buf + (uint32_t)(j * 32 + lane) * 4u, v[j]);
+                                ptx::st_shared_u32(wbuf + (uint32_t)(j * 32 + lane) * 4u, v[j]);
                         } else {
                             uint32_t u[W / 2];
                             pack_chunk<W>(f, u, p.out_kind);
 #pragma unroll
                             for (int j = 0; j < W; ++j)
-                                ptx::st_shared_u16(buf + (uint32_t)(j * 32 + lane) * 2u,
+                                ptx::st_shared_u16(wbuf + (uint32_t)(j * 32 + lane) * 2u,
                                                    (uint16_t)(u[j / 2] >> (16 * (j & 1))));
                         }
                         ptx::fence_async_smem();
                         __syncwarp();
                         if (lane == 0) {
-                            ptx::tma_store_3d(&tmC, sE + (buf - ptx::smem_addr(sE)),
+                            ptx::tma_store_3d(&tmC, sE + (wbuf - ptx::smem_addr(sE)),
                                               tp * 128 + quarter * 32, tq * BN + c * W, b);
                             ptx::bulk_commit();
                         }
+                        pending = true;
                     }
                 }
                 ptx::tc_fence_before();
@@ -433,7 +437,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             char* Cb = reinterpret_cast<char*>(p.C) +
                        (long long)b * p.sC * (p.out_kind == 2 ? 4 : 2);
 #pragma unroll 1
-            for (int c = 0; c < (BN + 31) / 32; ++c) {
+            for (int c = grp; c < (BN + 31) / 32; c += 2) {
                 uint32_t v[32];
                 if (BN >= 32) ptx::tmem_ld32(taddr + c * 32, v);
                 else ptx::tmem_ld16(taddr + c * 32, v);
@@ -484,8 +488,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t dst = ptx::mapa(
                 red_addr + (uint32_t)(((rank * rows) + (row - owner * rows)) * RS) * 4u, owner);
             const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16);
+            const int grp = (warp - kEpiWarp0) >> 2;
 #pragma unroll 1
-            for (int c = 0; c < (BN + 31) / 32; ++c) {
+            for (int c = grp; c < (BN + 31) / 32; c += 2) {
                 uint32_t v[32];
                 if (BN >= 32) ptx::tmem_ld32(taddr + c * 32, v);
                 else ptx::tmem_ld16(taddr + c * 32, v);
@@ -510,7 +515,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int n4 = BN / 4;
             const int slot = rows * RS;             // floats per source-rank slot
 #pragma unroll 1
-            for (int idx = et; idx < rows * n4; idx += 128) {
+            for (int idx = et; idx < rows * n4; idx += kEpiThreads) {
                 int rr, cc;
                 if (SWAP) { rr = idx % rows; cc = (idx / rows) * 4; }   // consecutive n
                 else { rr = idx / n4; cc = (idx % n4) * 4; }            // consecutive n
