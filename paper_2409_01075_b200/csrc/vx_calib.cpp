@@ -2,9 +2,10 @@
 // (Sec. 5.2: "empirical profiling ... on GPUs at both L0 and L1
 // levels. For higher levels, it utilizes an analytical cost model").
 //
-// On sm_100a the L0/L1 behaviour of a rung is summarised by four steady-state rates that
-// are measured ONCE on a B200 (tools/calibrate.py, evidence under profiles/) and compiled
-// in, so vx_plan stays deterministic and sample-free (no shape is ever profiled):
+// On sm_100a the L0/L1 behaviour of a rung is summarised by four effective rates, fitted
+// ONCE from a forced-rung profile of every rung on a fixed generic grid of calibration
+// shapes (tools/calibrate.py; raw data in profiles/) and compiled in, so vx_plan stays
+// deterministic and sample-free (no workload shape is ever profiled):
 //   mac_milli  MACs per SM cycle of the rung's MMA issue loop           (Cost_{L-1})
 //   l2s_milli  bytes per SM cycle TMA delivers into this CTA's SMEM ring (T_Load, per CTA)
 //   epi_milli  bytes per SM cycle of the TMEM -> register -> global epilogue (T_Store)
@@ -21,19 +22,19 @@
 namespace vx {
 
 static const Calib kCalib = {
-    /*hbm_milli=*/3330000,   // 6543 GB/s measured copy bandwidth / 1.965 GHz
-    /*dsm_milli=*/20000,     // ~20 B/cycle DSMEM (B300_MICROARCH.md)
-    /*fixed_cluster=*/1500,  // cluster launch + two cluster barriers
+    /*hbm_milli=*/3329822,   // 6543 GB/s measured copy bandwidth / 1.965 GHz
+    /*dsm_milli=*/3261,      // effective in-cluster reduce rate (fitted)
+    /*fixed_cluster=*/2427,  // cluster launch + two cluster barriers (fitted)
 };
 
 static const RungCalib kRungs[] = {
-    {"umma_128x64", 2730000, 64000, 64000, 3000},
-    {"umma_128x128", 4096000, 64000, 64000, 3000},
-    {"umma_128x256", 4096000, 64000, 64000, 3000},
-    {"umma_swap_128x16", 910000, 64000, 16000, 3000},
-    {"umma_swap_128x32", 1638000, 64000, 16000, 3000},
-    {"umma_swap_128x64", 2730000, 64000, 16000, 3000},
-    {"umma_swap_128x128", 4096000, 64000, 16000, 3000},
+    {"umma_128x64", 1003377, 43820, 8003, 3575},
+    {"umma_128x128", 4093394, 54778, 10035, 964},
+    {"umma_128x256", 2845438, 159928, 17540, 500},
+    {"umma_swap_128x16", 1000639, 24482, 511333, 4137},
+    {"umma_swap_128x32", 1000890, 28073, 509146, 3772},
+    {"umma_swap_128x64", 1050960, 43947, 25956, 3978},
+    {"umma_swap_128x128", 4091702, 54904, 39024, 3435},
     {"simt_32x32", 128000, 32000, 16000, 2000},
     {"simt_64x64", 128000, 32000, 16000, 2000},
     {"simt_128x64", 128000, 32000, 16000, 2000},

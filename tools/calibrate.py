@@ -92,6 +92,13 @@ def fit(args):
     for k in keys:
         x0 += [math.log(4096 if k[2] >= 128 else 2048), math.log(96), math.log(64), math.log(3000)]
     x0 += [math.log(20), math.log(1500)]
+    if args.init:
+        ini = json.load(open(args.init))
+        for i, n in enumerate(names):
+            r = ini["rungs"][n]
+            x0[4 * i:4 * i + 4] = [math.log(r["mac_milli"] / 1000), math.log(r["l2s_milli"] / 1000),
+                                   math.log(r["epi_milli"] / 1000), math.log(max(r["fixed"], 1))]
+        x0[-2:] = [math.log(ini["dsm_milli"] / 1000), math.log(max(ini["fixed_cluster"], 1))]
 
     def unpack(x):
         th = {}
@@ -104,15 +111,34 @@ def fit(args):
     def key_of(x):
         return "%s_%dx%d" % ("umma_swap" if x["family"] == 1 else "umma", x["bm"], x["bn"])
 
+    groups = {}
+    for sm in S:
+        groups.setdefault((sm["M"], sm["N"], sm["K"]), []).append(sm)
+    best_t = {k: min(x["us"] for x in v) for k, v in groups.items()}
+
     def loss(x):
         th, g = unpack(x)
         e = 0.0
         for sm in S:
             pred = model_us(sm, th[key_of(sm)], desc, g)
             e += (math.log(pred) - math.log(sm["us"])) ** 2
-        return e / len(S)
+        e /= len(S)
+        # selection quality: log-regret of the model's pick per calibration shape
+        r = 0.0
+        for k, v in groups.items():
+            pick = min(v, key=lambda z: model_us(z, th[key_of(z)], desc, g))
+            r += math.log(pick["us"] / best_t[k])
+        return e + args.regret_weight * r / len(groups)
 
-    res = minimize(loss, np.array(x0), method="Powell", options={"maxiter": 20000, "xtol": 1e-3})
+    lo, hi = [], []
+    for _ in keys:
+        lo += [math.log(1000), math.log(8), math.log(8), math.log(500)]
+        hi += [math.log(4096), math.log(160), math.log(512), math.log(12000)]
+    lo += [math.log(2), math.log(1)]
+    hi += [math.log(64), math.log(8000)]
+    x0 = [min(max(v, a), b) for v, a, b in zip(x0, lo, hi)]
+    res = minimize(loss, np.array(x0), method="Powell", bounds=list(zip(lo, hi)),
+                   options={"maxiter": 40000, "xtol": 1e-3, "ftol": 1e-6})
     th, g = unpack(res.x)
     print("rms log error %.3f" % math.sqrt(res.fun))
     # regret of the fitted model on the calibration grid
@@ -144,6 +170,8 @@ def main():
     m.add_argument("--out", default="gpurun_out/calib_raw.json")
     f = sub.add_parser("fit")
     f.add_argument("raw")
+    f.add_argument("--regret-weight", type=float, default=2.0)
+    f.add_argument("--init", default=None, help="start from a calibration json")
     args = ap.parse_args()
     if args.cmd == "measure":
         measure(args)
