@@ -209,6 +209,7 @@ def build_table(K: int, in_dtype: str, out_dtype: str, desc: dict) -> dict:
                     if s > 1 and bm * (bn + 4) * 4 > S * stage_bytes:
                         continue
                     splits.append(s)
+                splits.append(0)          # stream-K schedule over (tile, k-block) units (R19)
                 rungs.append({"family": swap, "cg": cg, "um": bm, "un": bn, "acc_stages": st,
                               "bm": bm, "bn": bn, "bk": bk, "stages": S, "swap": swap,
                               "splits": splits})
@@ -270,6 +271,9 @@ def rung_cost(rung: dict, s: int, batch: int, M: int, N: int, K: int,
     tm, tn = ceil_div(mt, bm), ceil_div(nt, bn)
     tiles = batch * tm * tn
     kb = ceil_div(K, bk)
+    if s == 0:
+        return _streamk_cost(rung, batch, M, N, K, mt, nt, tm, tn, tiles, kb, in_b, out_b,
+                             desc, calib, cal)
     trips = kb // s                                   # sizeof(TemporalLoop) at CTA level (R8)
     W = tiles * s                                     # sizeof(ParallelLoop) at grid level
     if rung["family"] == 2:
@@ -307,6 +311,30 @@ def rung_cost(rung: dict, s: int, batch: int, M: int, N: int, K: int,
         cost = level_cost(F, T) + cal["fixed"] + (calib["fixed_cluster"] if s > 1 else 0)
     return {"cost": cost, "tiles_m": tm, "tiles_n": tn, "tiles": tiles, "F": F,
             "grid": W if s > 1 or rung["family"] == 2 else min(tiles, slots),
+            "padded_work": batch * tm * bm * tn * bn}
+
+
+def _streamk_cost(rung, batch, M, N, K, mt, nt, tm, tn, tiles, kb, in_b, out_b, desc, calib,
+                  cal):
+    """Stream-K schedule (R19): G = min(resident CTAs, U) CTAs share the U = tiles x k-blocks
+    work units evenly in one wave (Eq. 3 gives F = 1); each CTA's temporal loop is
+    ceil(U/G) k-blocks (Eq. 2) touching at most ceil(units/kb)+1 tile segments, whose
+    epilogues overlap the loop except the last; a cut tile adds one partial write + read."""
+    bm, bn, bk = rung["bm"], rung["bn"], rung["bk"]
+    hbm = calib["hbm_milli"]
+    U = tiles * kb
+    G = min(desc["max_active_clusters"]["1"], U)
+    units = ceil_div(U, G)
+    segs = ceil_div(units, kb) + 1
+    inner = t_load(bm * bn * bk, cal["mac_milli"])
+    l_smem = t_load((bm + bn) * bk * in_b, cal["l2s_milli"])
+    l_hbm = t_load(in_b * batch * K * (mt + nt), units * hbm)
+    tl = max(l_smem, l_hbm)
+    t_main = temporal_cost(tl, units, inner, 0)
+    st = max(t_load(bm * bn * out_b, cal["epi_milli"]), t_load(out_b * batch * M * N, segs * hbm))
+    fix = t_load(2 * bm * bn * 4, calib["skfix_milli"])
+    cost = max(t_main, segs * st) + st + fix + cal["fixed"]
+    return {"cost": cost, "tiles_m": tm, "tiles_n": tn, "tiles": tiles, "F": 1, "grid": G,
             "padded_work": batch * tm * bm * tn * bn}
 
 

@@ -25,6 +25,7 @@ static const Calib kCalib = {
     /*hbm_milli=*/3329822,   // 6543 GB/s measured copy bandwidth / 1.965 GHz
     /*dsm_milli=*/3261,      // effective in-cluster reduce rate (fitted)
     /*fixed_cluster=*/2427,  // cluster launch + two cluster barriers (fitted)
+    /*skfix_milli=*/32000,   // stream-K partial write + read-back (round-1 estimate)
 };
 
 static const RungCalib kRungs[] = {

@@ -149,6 +149,27 @@ static vx_status make_map(CUtensorMap* map, const void* base, vx_dtype dt, int64
 
 static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// stream-K workspace: one partial slot (128 x 256 fp32) + one flag per SM, allocated once
+// per plan on its device (outside any graph capture: vx_plan allocates it eagerly)
+static size_t ws_bytes(const vx_plan_s* p) {
+    return (size_t)p->desc.sm_count * 128 * 256 * 4 + (size_t)p->desc.sm_count * 4 + 256;
+}
+static vx_status ensure_ws(const vx_plan_s* pc) {
+    vx_plan_s* p = const_cast<vx_plan_s*>(pc);
+    std::lock_guard<std::mutex> lk(p->ws_mu);
+    if (p->ws) return VX_OK;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    void* w = nullptr;
+    cudaError_t e = cudaMalloc(&w, ws_bytes(p));
+    if (e != cudaSuccess) return cuda_fail(e, "stream-K workspace cudaMalloc");
+    e = cudaMemset(w, 0, ws_bytes(p));
+    if (e != cudaSuccess) { cudaFree(w); return cuda_fail(e, "stream-K workspace memset"); }
+    p->ws = w;
+    p->ws_device = dev;
+    return VX_OK;
+}
+
 vx_status launch(const vx_plan_s* p, const vx_choice& ch, int64_t batch, int64_t M, int64_t N,
                  int64_t K, const void* A, int64_t sA, const void* B, int64_t sB, void* C,
                  int64_t sC, void* stream) {
@@ -195,7 +216,17 @@ vx_status launch(const vx_plan_s* p, const vx_choice& ch, int64_t batch, int64_t
     prm.tiles_q = ch.tiles_n;
     prm.num_tiles = (int)(batch * (int64_t)ch.tiles_m * ch.tiles_n);
     prm.kb_total = (int)cdiv(K, kBkTc);
-    prm.splits = ch.split;
+    prm.splits = ch.split > 0 ? ch.split : 1;
+    prm.streamk = ch.split == 0;
+    prm.ws = nullptr;
+    prm.flags = nullptr;
+    if (prm.streamk) {
+        s = ensure_ws(p);
+        if (s != VX_OK) return s;
+        prm.ws = reinterpret_cast<float*>(p->ws);
+        prm.flags = reinterpret_cast<int*>(reinterpret_cast<char*>(p->ws) +
+                                           (size_t)p->desc.sm_count * 128 * 256 * 4);
+    }
     prm.stages = r.stages;
     prm.out_kind = p->out == VX_BF16 ? 0 : p->out == VX_FP16 ? 1 : 2;
     const uint32_t fmt = p->in == VX_BF16 ? 1u : 0u;
@@ -228,7 +259,7 @@ vx_status launch(const vx_plan_s* p, const vx_choice& ch, int64_t batch, int64_t
     cfg.stream = st;
     cudaLaunchAttribute attr[2];
     unsigned na = 0;
-    if (ch.split > 1) {
+    if (ch.split > 1) {   // split-K cluster (split 0 = stream-K, no cluster)
         attr[na].id = cudaLaunchAttributeClusterDimension;
         attr[na].val.clusterDim.x = (unsigned)ch.split;
         attr[na].val.clusterDim.y = 1;
@@ -254,6 +285,10 @@ vx_status launch(const vx_plan_s* p, const vx_choice& ch, int64_t batch, int64_t
 }
 
 vx_status prepare_kernels(const vx_plan_s* p) {
+    if (p->in != VX_FP32) {
+        vx_status s = ensure_ws(p);
+        if (s != VX_OK) return s;
+    }
     for (const vx::Rung& r : p->rungs) {
         if (r.family == kSimt) continue;
         UmmaFn fn = umma_fn(r.family, r.bn, p->bl == VX_B_KN);
@@ -265,6 +300,16 @@ vx_status prepare_kernels(const vx_plan_s* p) {
 }
 
 }  // namespace vx
+
+vx_plan_s::~vx_plan_s() {
+    if (ws) {
+        int cur = 0;
+        cudaGetDevice(&cur);
+        cudaSetDevice(ws_device);
+        cudaFree(ws);
+        cudaSetDevice(cur);
+    }
+}
 
 using namespace vx;
 

@@ -4,6 +4,7 @@
 
 #include <atomic>
 #include <memory>
+#include <mutex>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -39,7 +40,7 @@ struct Rung {
 };
 
 struct Calib {
-    int64_t hbm_milli, dsm_milli, fixed_cluster;
+    int64_t hbm_milli, dsm_milli, fixed_cluster, skfix_milli;
 };
 
 struct RungCalib {
@@ -72,6 +73,11 @@ struct vx_plan_s {
     static constexpr int64_t kMemo = 16384;
     std::vector<vx_choice> memo;
     std::unique_ptr<std::atomic<uint8_t>[]> memo_state;
+    // stream-K workspace (device): sm_count partial slots of 128 x 256 fp32 + flags
+    void* ws = nullptr;
+    int ws_device = -1;
+    std::mutex ws_mu;
+    ~vx_plan_s();
 };
 
 namespace vx {

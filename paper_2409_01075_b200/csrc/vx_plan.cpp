@@ -143,6 +143,7 @@ static vx_status build_rungs(vx_plan_s* p) {
                     if (s > 1 && (int64_t)c.bm * (c.bn + 4) * 4 > c.S * stage) continue;
                     r.splits.push_back(s);
                 }
+                r.splits.push_back(0);  // stream-K over (tile, k-block) units (R19)
                 rungs.push_back(r);
             }
         }
@@ -200,6 +201,27 @@ static void rung_cost(const vx_plan_s* p, const Rung& r, int s, int64_t batch, i
     const int64_t tm = cdiv(mt, bm), tn = cdiv(nt, bn);
     const int64_t tiles = batch * tm * tn;
     const int64_t kb = cdiv(K, bk);
+    if (s == 0) {
+        // stream-K (R19): G resident CTAs share U = tiles x k-blocks units evenly; one wave
+        const int64_t U = tiles * kb;
+        const int64_t G = std::min<int64_t>(d.max_active_clusters[0], U);
+        const int64_t units = cdiv(U, G);                       // temporal loop per CTA
+        const int64_t segs = cdiv(units, kb) + 1;               // tile segments per CTA (bound)
+        const int64_t inner = t_move(bm * bn * bk, r.mac_milli);
+        const int64_t l_smem = t_move((bm + bn) * bk * in_b, r.l2s_milli);
+        const int64_t l_hbm = t_move((int64_t)in_b * batch * K * (mt + nt), units * cal.hbm_milli);
+        const int64_t tl = std::max(l_smem, l_hbm);
+        const int64_t tm_ = eq2(tl, units, inner, 0);
+        const int64_t st = std::max(t_move(bm * bn * out_b, r.epi_milli),
+                                    t_move((int64_t)out_b * batch * M * N, segs * cal.hbm_milli));
+        const int64_t fix = t_move(2 * bm * bn * 4, cal.skfix_milli);
+        o->rung_id = r.rung_id; o->split = 0; o->family = r.family; o->swap = r.swap;
+        o->bm = r.bm; o->bn = r.bn; o->stages = r.stages;
+        o->tiles_m = (int32_t)tm; o->tiles_n = (int32_t)tn; o->grid = (int32_t)G;
+        o->cluster = 1; o->reserved = 0;
+        o->cost = std::max(tm_, segs * st) + st + fix + r.fixed;
+        return;
+    }
     const int64_t trips = kb / s;            // sizeof(TemporalLoop) at the CTA level (R8)
     const int64_t W = tiles * s;             // sizeof(ParallelLoop) at the grid level
     int64_t slots;
@@ -372,7 +394,7 @@ vx_status vx_plan(int64_t N, int64_t K, vx_dtype in, vx_dtype out, vx_blayout bl
 }
 
 vx_status vx_plan_destroy(vx_plan_t plan) {
-    delete plan;
+    delete plan;   // ~vx_plan_s releases the stream-K workspace (vx_dispatch.cu)
     return VX_OK;
 }
 
@@ -394,11 +416,11 @@ vx_status vx_plan_dump(vx_plan_t p, char* buf, size_t cap, size_t* need) {
     snprintf(tmp, sizeof tmp,
              "{\"abi\":%d,\"N\":%lld,\"K\":%lld,\"in\":\"%s\",\"out\":\"%s\",\"b_layout\":\"%s\","
              "\"levels\":{\"l0\":%lld,\"l1\":%lld,\"l2\":%lld,\"l3\":%lld},"
-             "\"calib\":{\"hbm_milli\":%lld,\"dsm_milli\":%lld,\"fixed_cluster\":%lld},\"rungs\":[",
+             "\"calib\":{\"hbm_milli\":%lld,\"dsm_milli\":%lld,\"fixed_cluster\":%lld,\"skfix_milli\":%lld},\"rungs\":[",
              VX_ABI_VERSION, (long long)p->N, (long long)p->K, dt_name(p->in), dt_name(p->out),
              p->bl == VX_B_KN ? "kn" : "nk", (long long)p->counts.l0, (long long)p->counts.l1,
              (long long)p->counts.l2, (long long)p->counts.l3, (long long)c.hbm_milli,
-             (long long)c.dsm_milli, (long long)c.fixed_cluster);
+             (long long)c.dsm_milli, (long long)c.fixed_cluster, (long long)c.skfix_milli);
     s += tmp;
     for (size_t i = 0; i < p->rungs.size(); ++i) {
         const Rung& r = p->rungs[i];

@@ -31,6 +31,11 @@
 
 namespace vx {
 
+constexpr int kEpiWarp0 = 2;
+constexpr int kEpiWarps = 8;   // two warps per TMEM lane quarter, splitting the column chunks
+constexpr int kEpiThreads = kEpiWarps * 32;
+constexpr int kThreads = kEpiWarp0 * 32 + kEpiThreads;
+
 struct UmmaParams {
     int M, N;                 // logical GEMM rows / cols (per batch)
     int tiles_p, tiles_q;     // tiles along the UMMA-M (P) and UMMA-N (Q) axes
@@ -46,7 +51,72 @@ struct UmmaParams {
     long long sC;             // elements between batches of C
     unsigned long long* trace;  // optional per-CTA phase timestamps (VX_TRACE), else null
     int dbg;                    // debug bits (VX_DEBUG_FLAGS): 1 skip push, 2 skip reduce, 4 skip C store
+    int streamk;                // 1: stream-K schedule over (tile, k-block) units
+    float* ws;                  // stream-K partial slots [gridDim.x][128][BN] fp32 (plan-owned)
+    int* flags;                 // stream-K slot-ready flags [gridDim.x] (0 between launches)
 };
+
+// ---- work assignment (the L3 schedule of the rung) ---------------------------------------
+// persistent: tiles blockIdx.x, +gridDim.x, ... each over the whole K range
+// split:      one tile per cluster, K range [rank*K/s, (rank+1)*K/s)
+// stream-K:   CTA c owns units [c*U/G, (c+1)*U/G) of U = tiles x k-blocks (tile-major);
+//             a tile cut between CTAs is finished by the CTA holding its k-block 0, which
+//             adds the other CTAs' fp32 partials in CTA order (deterministic)
+struct WorkIter {
+    long long u, u1;       // stream-K unit cursor / end
+    int tile, step;        // persistent / split
+    int ka, kn;            // split K range
+    __device__ __forceinline__ WorkIter(const UmmaParams& p, int rank) {
+        if (p.streamk) {
+            const long long U = (long long)p.num_tiles * p.kb_total;
+            u = (long long)blockIdx.x * U / gridDim.x;
+            u1 = (long long)(blockIdx.x + 1) * U / gridDim.x;
+        } else if (p.splits > 1) {
+            tile = blockIdx.x / p.splits;
+            step = p.num_tiles;
+            kn = p.kb_total / p.splits;
+            ka = rank * kn;
+        } else {
+            tile = blockIdx.x;
+            step = gridDim.x;
+            ka = 0;
+            kn = p.kb_total;
+        }
+    }
+    // next work item: tile and its k-block range [k0, k0+nk); false when done
+    __device__ __forceinline__ bool next(const UmmaParams& p, int& t, int& k0, int& nk) {
+        if (p.streamk) {
+            if (u >= u1) return false;
+            t = (int)(u / p.kb_total);
+            k0 = (int)(u - (long long)t * p.kb_total);
+            const long long rest = u1 - u;
+            nk = (int)min((long long)(p.kb_total - k0), rest);
+            u += nk;
+            return true;
+        }
+        if (tile >= p.num_tiles) return false;
+        t = tile;
+        k0 = ka;
+        nk = kn;
+        tile += step;
+        return true;
+    }
+};
+
+// first unit of CTA c under the stream-K split (same formula as WorkIter)
+__device__ __forceinline__ long long sk_first(long long c, long long U, long long G) { return c * U / G; }
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void epi_bar() {   // named barrier over the 8 epilogue warps
+    asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+}
 
 // phase trace (tracing aux subsystem): %globaltimer (ns) at fixed points, 8 slots per CTA
 __device__ __forceinline__ void trace_at(const UmmaParams& p, int slot) {
@@ -57,10 +127,6 @@ __device__ __forceinline__ void trace_at(const UmmaParams& p, int slot) {
     }
 }
 
-constexpr int kEpiWarp0 = 2;
-constexpr int kEpiWarps = 8;   // two warps per TMEM lane quarter, splitting the column chunks
-constexpr int kEpiThreads = kEpiWarps * 32;
-constexpr int kThreads = kEpiWarp0 * 32 + kEpiThreads;
 constexpr int kGroupP = 16;   // raster: 16 P-tiles x all Q-tiles per group (L2 reuse)
 
 template <int BN>
@@ -200,6 +266,33 @@ __device__ __forceinline__ void store_col_chunk(char* Cb, long long ldc, int col
     }
 }
 
+// stream-K: add the fp32 partials of CTAs c0..c1 (in that order) for accumulator row `row`,
+// columns col0 .. col0+W-1, into the W values held as fp32 bits in v
+template <int W>
+__device__ __forceinline__ void add_partials(uint32_t* v, const float* ws, int c0, int c1, int row,
+                                             int col0, int bn) {
+#pragma unroll 1
+    for (int j = c0; j <= c1; ++j) {
+        const float* src = ws + ((long long)j * 128 + row) * bn + col0;
+#pragma unroll
+        for (int i = 0; i < W; i += 4) {
+            const float4 t = __ldcg(reinterpret_cast<const float4*>(src + i));
+            v[i] = __float_as_uint(__uint_as_float(v[i]) + t.x);
+            v[i + 1] = __float_as_uint(__uint_as_float(v[i + 1]) + t.y);
+            v[i + 2] = __float_as_uint(__uint_as_float(v[i + 2]) + t.z);
+            v[i + 3] = __float_as_uint(__uint_as_float(v[i + 3]) + t.w);
+        }
+    }
+}
+
+// stream-K: every epilogue warp has consumed slots c0..c1 -> clear their flags for the next
+// launch (each slot is produced and consumed exactly once per launch)
+__device__ __forceinline__ void sk_reset(const UmmaParams& p, int c0, int c1) {
+    epi_bar();
+    if (threadIdx.x == kEpiWarp0 * 32)
+        for (int j = c0; j <= c1; ++j) p.flags[j] = 0;
+}
+
 // SWAP: P = B, Q = A.  P_MN / Q_MN: that operand is MN-major in SMEM (B stored K x N).
 template <int BN, bool SWAP, bool P_MN, bool Q_MN>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -250,14 +343,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // kernel under PDL; no global memory is touched before this point
     ptx::grid_dep_wait();
 
-    // work assignment: split mode -> one tile per cluster, K range by cluster rank;
-    // persistent mode -> tiles blockIdx.x, +gridDim.x, ...; whole K range
     const bool split = p.splits > 1;
     const int rank = split ? (int)(blockIdx.x % p.splits) : 0;
-    const int tile0 = split ? (int)(blockIdx.x / p.splits) : (int)blockIdx.x;
-    const int tstep = split ? p.num_tiles : (int)gridDim.x;
-    const int kb_n = p.kb_total / p.splits;
-    const int kb0 = rank * kb_n;
+    const int tile0 = split ? (int)(blockIdx.x / p.splits) : (int)blockIdx.x;  // split mode
 
     if (warp == 0) {
         if (lane == 0) {
@@ -265,10 +353,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t pol = ptx::policy_evict_last();
             int stage = 0;
             uint32_t phase = 0;
-            for (int tile = tile0; tile < p.num_tiles; tile += tstep) {
+            WorkIter wi(p, rank);
+            int tile, k0, nk;
+            while (wi.next(p, tile, k0, nk)) {
                 int b, tp, tq;
                 decode_tile(tile, p.tiles_p, p.tiles_q, b, tp, tq);
-                for (int kb = kb0; kb < kb0 + kb_n; ++kb) {
+                for (int kb = k0; kb < k0 + nk; ++kb) {
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
                     ptx::mbar_arrive_expect_tx(&full[stage], kP + kQ);
                     uint8_t* dP = sP + stage * kP;
@@ -301,13 +391,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             int stage = 0;
             uint32_t phase = 0;
             int it = 0;
-            for (int tile = tile0; tile < p.num_tiles; tile += tstep, ++it) {
+            WorkIter wi(p, rank);
+            int tile, k0, nk;
+            for (; wi.next(p, tile, k0, nk); ++it) {
                 const int acc = it & 1;
                 const uint32_t acc_phase = (it >> 1) & 1;
                 ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
                 ptx::tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
-                for (int i = 0; i < kb_n; ++i) {
+                for (int i = 0; i < nk; ++i) {
                     ptx::mbar_wait(&full[stage], phase);
                     ptx::tc_fence_after();
                     if (it == 0 && i == 0) trace_at(p, 3);
@@ -339,7 +431,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t wbuf = ptx::smem_addr(sE) + (uint32_t)(warp - kEpiWarp0) * 4096u;
         bool pending = false;                  // a TMA store still reads this warp's buffer
         int it = 0;
-        for (int tile = tile0; tile < p.num_tiles; tile += tstep, ++it) {
+        WorkIter wi(p, rank);
+        int tile, k0, nk;
+        const long long U = (long long)p.num_tiles * p.kb_total;
+        for (; wi.next(p, tile, k0, nk); ++it) {
             int b, tp, tq;
             decode_tile(tile, p.tiles_p, p.tiles_q, b, tp, tq);
             const int acc = it & 1;
@@ -349,6 +444,42 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (it == 0 && threadIdx.x == kEpiWarp0 * 32) trace_at(p, 5);
             const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
             if (split) break;  // split mode: the accumulator is read after the cluster barrier
+            // ---- stream-K: a cut tile ----------------------------------------------------
+            int c_first = 0, c_last = -1;          // CTAs whose partials this CTA adds
+            if (p.streamk && k0 > 0) {
+                // not the owner: park the fp32 partial in this CTA's slot and publish it
+                float* slot = p.ws + (long long)blockIdx.x * 128 * BN + (long long)row * BN;
+#pragma unroll 1
+                for (int c = grp; c < (BN + 31) / 32; c += 2) {
+                    uint32_t v[32];
+                    if (BN >= 32) ptx::tmem_ld32(taddr + c * 32, v);
+                    else ptx::tmem_ld16(taddr + c * 32, v);
+                    ptx::tmem_wait_ld();
+                    constexpr int W = BN >= 32 ? 32 : BN;
+#pragma unroll
+                    for (int j = 0; j < W; j += 4)
+                        *reinterpret_cast<uint4*>(slot + c * 32 + j) = make_uint4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                }
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+                __threadfence();
+                epi_bar();
+                if (threadIdx.x == kEpiWarp0 * 32) st_release(p.flags + blockIdx.x, 1);
+                continue;
+            }
+            if (p.streamk && nk < p.kb_total) {
+                // owner of a cut tile: the rest of its K range sits in CTAs c+1 .. c_last
+                c_first = blockIdx.x + 1;
+                const long long last_unit = (long long)(tile + 1) * p.kb_total - 1;
+                c_last = blockIdx.x;
+                while (c_last + 1 < (int)gridDim.x && sk_first(c_last + 1, U, gridDim.x) <= last_unit)
+                    ++c_last;
+                if (lane == 0)
+                    for (int j = c_first; j <= c_last; ++j)
+                        while (ld_acquire(p.flags + j) == 0) { }
+                __syncwarp();
+            }
             if (p.vec && !(p.dbg & 8)) {
                 // TMEM -> registers -> swizzled SMEM staging -> TMA bulk store (full lines,
                 // asynchronous, M/N tails clipped by the tensor map)
@@ -366,6 +497,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             uint32_t v[32];
                             ptx::tmem_ld32(taddr + k * CW, v);
                             ptx::tmem_wait_ld();
+                            add_partials<32>(v, p.ws, c_first, c_last, row, k * CW, BN);
 #pragma unroll
                             for (int j = 0; j < 8; ++j)
                                 ptx::st_shared_v4(rowa + (((uint32_t)(j ^ (lane & 7))) << 4),
@@ -376,6 +508,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             ptx::tmem_ld32(taddr + k * CW + 32,
                                            *reinterpret_cast<uint32_t(*)[32]>(v + 32));
                             ptx::tmem_wait_ld();
+                            add_partials<64>(v, p.ws, c_first, c_last, row, k * CW, BN);
                             uint32_t u[32];
                             pack_chunk<64>(reinterpret_cast<const float*>(v), u, p.out_kind);
 #pragma unroll
@@ -404,6 +537,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         if (BN >= 32) ptx::tmem_ld32(taddr + c * 32, v);
                         else ptx::tmem_ld16(taddr + c * 32, v);
                         ptx::tmem_wait_ld();
+                        add_partials<W>(v, p.ws, c_first, c_last, row, c * 32, BN);
                         const float* f = reinterpret_cast<const float*>(v);
                         // staging tile [W m-rows][32 n] (row pitch 32*ob bytes), lane = n
                         if (ob == 4) {
@@ -431,6 +565,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+                if (c_last >= c_first) sk_reset(p, c_first, c_last);
                 continue;
             }
             const int pr = tp * 128 + row;  // global index on the P axis
@@ -443,6 +578,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 else ptx::tmem_ld16(taddr + c * 32, v);
                 ptx::tmem_wait_ld();
                 constexpr int W = BN >= 32 ? 32 : BN;
+                add_partials<W>(v, p.ws, c_first, c_last, row, c * 32, BN);
                 const float* f = reinterpret_cast<const float*>(v);
                 if (p.dbg & 8) {
                     if (f[0] == 12345.f) store1(Cb, 0, f[1], p.out_kind);
@@ -462,6 +598,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+            if (c_last >= c_first) sk_reset(p, c_first, c_last);
         }
         if (lane == 0) ptx::bulk_wait<0>();   // TMA stores complete before the CTA retires
     }

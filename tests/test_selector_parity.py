@@ -47,7 +47,8 @@ def test_tables_identical(K, io):
 
 def test_calibration_copies_agree():
     d = vx.Plan(4096, 4096, "bf16", "bf16", "nk", desc=DESC).dump()
-    assert d["calib"] == {k: CAL[k] for k in ("hbm_milli", "dsm_milli", "fixed_cluster")}
+    assert d["calib"] == {k: CAL[k] for k in ("hbm_milli", "dsm_milli", "fixed_cluster",
+                                              "skfix_milli")}
     for r in d["rungs"]:
         key = "%s_%dx%d" % (S.FAMILY_NAMES[r["family"]], r["bm"], r["bn"])
         for f in ("mac_milli", "l2s_milli", "epi_milli", "fixed"):
