@@ -288,7 +288,8 @@ def rung_cost(rung: dict, s: int, batch: int, M: int, N: int, K: int,
         l_smem = t_load((bm + bn) * bk * in_b * occ, cal["l2s_milli"])
     else:
         inner = t_load(bm * bn * bk, cal["mac_milli"])          # Cost_{L-1}, empirical tier
-        l_smem = t_load((bm + bn) * bk * in_b, cal["l2s_milli"])
+        # rows past M / N are zero-filled by TMA without memory traffic (R10)
+        l_smem = t_load((min(bm, mt) + min(bn, nt)) * bk * in_b, cal["l2s_milli"])
     # HBM share of one k-step: the grid's unique operand bytes leave HBM once, spread over
     # F waves x trips k-steps that all run at the chip bandwidth (R10)
     uniq = in_b * batch * K * (mt + nt)
@@ -327,7 +328,7 @@ def _streamk_cost(rung, batch, M, N, K, mt, nt, tm, tn, tiles, kb, in_b, out_b, 
     units = ceil_div(U, G)
     segs = ceil_div(units, kb) + 1
     inner = t_load(bm * bn * bk, cal["mac_milli"])
-    l_smem = t_load((bm + bn) * bk * in_b, cal["l2s_milli"])
+    l_smem = t_load((min(bm, mt) + min(bn, nt)) * bk * in_b, cal["l2s_milli"])
     l_hbm = t_load(in_b * batch * K * (mt + nt), units * hbm)
     tl = max(l_smem, l_hbm)
     t_main = temporal_cost(tl, units, inner, 0)

@@ -208,7 +208,7 @@ static void rung_cost(const vx_plan_s* p, const Rung& r, int s, int64_t batch, i
         const int64_t units = cdiv(U, G);                       // temporal loop per CTA
         const int64_t segs = cdiv(units, kb) + 1;               // tile segments per CTA (bound)
         const int64_t inner = t_move(bm * bn * bk, r.mac_milli);
-        const int64_t l_smem = t_move((bm + bn) * bk * in_b, r.l2s_milli);
+        const int64_t l_smem = t_move((std::min(bm, mt) + std::min(bn, nt)) * bk * in_b, r.l2s_milli);
         const int64_t l_hbm = t_move((int64_t)in_b * batch * K * (mt + nt), units * cal.hbm_milli);
         const int64_t tl = std::max(l_smem, l_hbm);
         const int64_t tm_ = eq2(tl, units, inner, 0);
@@ -244,7 +244,8 @@ static void rung_cost(const vx_plan_s* p, const Rung& r, int s, int64_t batch, i
         l_smem = t_move((bm + bn) * bk * in_b * occ, r.l2s_milli);
     } else {
         inner = t_move(bm * bn * bk, r.mac_milli);           // Cost_{L-1}
-        l_smem = t_move((bm + bn) * bk * in_b, r.l2s_milli);
+        // rows past M / N are zero-filled by TMA without memory traffic (R10)
+        l_smem = t_move((std::min(bm, mt) + std::min(bn, nt)) * bk * in_b, r.l2s_milli);
     }
     const int64_t uniq = (int64_t)in_b * batch * K * (mt + nt);
     const int64_t l_hbm = t_move(uniq, F * trips * cal.hbm_milli);   // R10

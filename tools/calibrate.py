@@ -59,12 +59,23 @@ def model_us(sm, th, desc, g):
     tm, tn = -(-mt // bm), -(-nt // bn)
     tiles = tm * tn
     kb = -(-K // bk)
-    trips = kb // s
-    W = tiles * s
-    slots = desc["max_active_clusters"][str(s)] * s
+    trips = kb // max(s, 1)
+    W = tiles * max(s, 1)
+    slots = desc["max_active_clusters"][str(max(s, 1))] * max(s, 1)
     F = -(-W // slots)
     c = bm * bn * bk / th["mac"]
-    l = max((bm + bn) * bk * 2 / th["l2s"], 2 * K * (mt + nt) / (F * trips * g["hbm"]))
+    ls = (min(bm, mt) + min(bn, nt)) * bk * 2 / th["l2s"]
+    if s == 0:   # stream-K (R19)
+        U = tiles * kb
+        G = min(desc["max_active_clusters"]["1"], U)
+        units = -(-U // G)
+        segs = -(-units // kb) + 1
+        l = max(ls, 2 * K * (mt + nt) / (units * g["hbm"]))
+        tm_ = l + (units - 1) * max(l, c) + c
+        st = max(bm * bn * 2 / th["epi"], 2 * M * N / (segs * g["hbm"]))
+        cyc = max(tm_, segs * st) + st + 2 * bm * bn * 4 / g["skfix"] + th["fixed"]
+        return cyc / (CLOCK_GHZ * 1e3)
+    l = max(ls, 2 * K * (mt + nt) / (F * trips * g["hbm"]))
     st = max(bm * bn * 2 / (s * th["epi"]), 2 * M * N / (F * g["hbm"]))
     if s > 1:
         st += (s - 1) * bm * bn * 4 / (s * g["dsm"])
@@ -91,21 +102,22 @@ def fit(args):
     x0 = []
     for k in keys:
         x0 += [math.log(4096 if k[2] >= 128 else 2048), math.log(96), math.log(64), math.log(3000)]
-    x0 += [math.log(20), math.log(1500)]
+    x0 += [math.log(20), math.log(1500), math.log(32)]
     if args.init:
         ini = json.load(open(args.init))
         for i, n in enumerate(names):
             r = ini["rungs"][n]
             x0[4 * i:4 * i + 4] = [math.log(r["mac_milli"] / 1000), math.log(r["l2s_milli"] / 1000),
                                    math.log(r["epi_milli"] / 1000), math.log(max(r["fixed"], 1))]
-        x0[-2:] = [math.log(ini["dsm_milli"] / 1000), math.log(max(ini["fixed_cluster"], 1))]
+        x0[-3:] = [math.log(ini["dsm_milli"] / 1000), math.log(max(ini["fixed_cluster"], 1)),
+                   math.log(ini.get("skfix_milli", 32000) / 1000)]
 
     def unpack(x):
         th = {}
         for i, n in enumerate(names):
             th[n] = dict(mac=math.exp(x[4 * i]), l2s=math.exp(x[4 * i + 1]),
                          epi=math.exp(x[4 * i + 2]), fixed=math.exp(x[4 * i + 3]))
-        g = dict(hbm=hbm, dsm=math.exp(x[-2]), fixed_cluster=math.exp(x[-1]))
+        g = dict(hbm=hbm, dsm=math.exp(x[-3]), fixed_cluster=math.exp(x[-2]), skfix=math.exp(x[-1]))
         return th, g
 
     def key_of(x):
@@ -134,8 +146,8 @@ def fit(args):
     for _ in keys:
         lo += [math.log(1000), math.log(8), math.log(8), math.log(500)]
         hi += [math.log(4096), math.log(160), math.log(512), math.log(12000)]
-    lo += [math.log(2), math.log(1)]
-    hi += [math.log(64), math.log(8000)]
+    lo += [math.log(2), math.log(1), math.log(1)]
+    hi += [math.log(64), math.log(8000), math.log(256)]
     x0 = [min(max(v, a), b) for v, a, b in zip(x0, lo, hi)]
     res = minimize(loss, np.array(x0), method="Powell", bounds=list(zip(lo, hi)),
                    options={"maxiter": 40000, "xtol": 1e-3, "ftol": 1e-6})
@@ -153,7 +165,8 @@ def fit(args):
     print("calibration-grid regret geomean %.4f worst %.4f" % (
         math.exp(sum(math.log(r) for r in regrets) / len(regrets)), min(regrets)))
     out = {"hbm_milli": int(round(hbm * 1000)), "dsm_milli": int(round(g["dsm"] * 1000)),
-           "fixed_cluster": int(round(g["fixed_cluster"])), "rungs": {}}
+           "fixed_cluster": int(round(g["fixed_cluster"])),
+           "skfix_milli": int(round(g["skfix"] * 1000)), "rungs": {}}
     for n in names:
         t = th[n]
         out["rungs"][n] = {"mac_milli": int(round(t["mac"] * 1000)),
