@@ -23,19 +23,19 @@ namespace vx {
 
 static const Calib kCalib = {
     /*hbm_milli=*/3329822,   // 6543 GB/s measured copy bandwidth / 1.965 GHz
-    /*dsm_milli=*/3261,      // effective in-cluster reduce rate (fitted)
-    /*fixed_cluster=*/2427,  // cluster launch + two cluster barriers (fitted)
-    /*skfix_milli=*/32000,   // stream-K partial write + read-back (round-1 estimate)
+    /*dsm_milli=*/3012,      // effective in-cluster reduce rate (fitted)
+    /*fixed_cluster=*/540,  // cluster launch + two cluster barriers (fitted)
+    /*skfix_milli=*/2090,   // stream-K partial write + read-back (fitted)
 };
 
 static const RungCalib kRungs[] = {
-    {"umma_128x64", 1003377, 43820, 8003, 3575},
-    {"umma_128x128", 4093394, 54778, 10035, 964},
-    {"umma_128x256", 2845438, 159928, 17540, 500},
-    {"umma_swap_128x16", 1000639, 24482, 511333, 4137},
-    {"umma_swap_128x32", 1000890, 28073, 509146, 3772},
-    {"umma_swap_128x64", 1050960, 43947, 25956, 3978},
-    {"umma_swap_128x128", 4091702, 54904, 39024, 3435},
+    {"umma_128x64", 1080625, 31687, 8421, 6364},
+    {"umma_128x128", 1604274, 90452, 15160, 2127},
+    {"umma_128x256", 2973207, 159915, 15404, 500},
+    {"umma_swap_128x16", 1000639, 35786, 8004, 6133},
+    {"umma_swap_128x32", 1000639, 27018, 8005, 5698},
+    {"umma_swap_128x64", 1000602, 34658, 8006, 4920},
+    {"umma_swap_128x128", 2245181, 58716, 9467, 6839},
     {"simt_32x32", 128000, 32000, 16000, 2000},
     {"simt_64x64", 128000, 32000, 16000, 2000},
     {"simt_128x64", 128000, 32000, 16000, 2000},
