@@ -50,7 +50,9 @@ struct UmmaParams {
     long long ldc;            // elements between rows of C
     long long sC;             // elements between batches of C
     unsigned long long* trace;  // optional per-CTA phase timestamps (VX_TRACE), else null
-    int dbg;                    // debug bits (VX_DEBUG_FLAGS): 1 skip push, 2 skip reduce, 4 skip C store
+    int dbg;                    // debug bits (VX_DEBUG_FLAGS): 1 skip split push, 2 skip split
+                                // reduce, 4 skip split C store, 8 skip epilogue stores,
+                                // 32 skip stream-K fix-up (timing experiments only)
     int streamk;                // 1: stream-K schedule over (tile, k-block) units
     float* ws;                  // stream-K partial slots [gridDim.x][128][BN] fp32 (plan-owned)
     int* flags;                 // stream-K slot-ready flags [gridDim.x] (0 between launches)
@@ -273,10 +275,11 @@ __device__ __forceinline__ void add_partials(uint32_t* v, const float* ws, int c
                                              int col0, int bn) {
 #pragma unroll 1
     for (int j = c0; j <= c1; ++j) {
-        const float* src = ws + ((long long)j * 128 + row) * bn + col0;
+        // slot layout [col/4][row][4]: a warp's 32 rows read 512 contiguous bytes
+        const float* src = ws + (long long)j * 128 * bn + ((long long)(col0 / 4) * 128 + row) * 4;
 #pragma unroll
         for (int i = 0; i < W; i += 4) {
-            const float4 t = __ldcg(reinterpret_cast<const float4*>(src + i));
+            const float4 t = __ldcg(reinterpret_cast<const float4*>(src + i * 128));
             v[i] = __float_as_uint(__uint_as_float(v[i]) + t.x);
             v[i + 1] = __float_as_uint(__uint_as_float(v[i + 1]) + t.y);
             v[i + 2] = __float_as_uint(__uint_as_float(v[i + 2]) + t.z);
@@ -446,9 +449,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (split) break;  // split mode: the accumulator is read after the cluster barrier
             // ---- stream-K: a cut tile ----------------------------------------------------
             int c_first = 0, c_last = -1;          // CTAs whose partials this CTA adds
-            if (p.streamk && k0 > 0) {
+            if (p.streamk && k0 > 0 && !(p.dbg & 32)) {
                 // not the owner: park the fp32 partial in this CTA's slot and publish it
-                float* slot = p.ws + (long long)blockIdx.x * 128 * BN + (long long)row * BN;
+                // slot layout [col/4][row][4] (coalesced across the warp's rows)
+                float* slot = p.ws + (long long)blockIdx.x * 128 * BN + (long long)row * 4;
 #pragma unroll 1
                 for (int c = grp; c < (BN + 31) / 32; c += 2) {
                     uint32_t v[32];
@@ -458,27 +462,36 @@ __global__ void __launch_bounds__(kThreads, 1)
                     constexpr int W = BN >= 32 ? 32 : BN;
 #pragma unroll
                     for (int j = 0; j < W; j += 4)
-                        *reinterpret_cast<uint4*>(slot + c * 32 + j) = make_uint4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                        __stcg(reinterpret_cast<uint4*>(slot + (long long)((c * 32 + j) / 4) * 128 * 4),
+                               make_uint4(v[j], v[j + 1], v[j + 2], v[j + 3]));
                 }
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
                 __threadfence();
                 epi_bar();
-                if (threadIdx.x == kEpiWarp0 * 32) st_release(p.flags + blockIdx.x, 1);
+                if (threadIdx.x == kEpiWarp0 * 32) {
+                    __threadfence();
+                    atomicExch(p.flags + blockIdx.x, 1);
+                }
                 continue;
             }
-            if (p.streamk && nk < p.kb_total) {
+            if (p.streamk && nk < p.kb_total && !(p.dbg & 32)) {
                 // owner of a cut tile: the rest of its K range sits in CTAs c+1 .. c_last
                 c_first = blockIdx.x + 1;
                 const long long last_unit = (long long)(tile + 1) * p.kb_total - 1;
                 c_last = blockIdx.x;
                 while (c_last + 1 < (int)gridDim.x && sk_first(c_last + 1, U, gridDim.x) <= last_unit)
                     ++c_last;
-                if (lane == 0)
+                // one thread acquires the contributors' flags (backing off between polls so
+                // the publishers' stores are not starved); the named barrier then orders
+                // every epilogue thread's partial reads after that acquire
+                if (threadIdx.x == kEpiWarp0 * 32) {
                     for (int j = c_first; j <= c_last; ++j)
-                        while (ld_acquire(p.flags + j) == 0) { }
-                __syncwarp();
+                        while (atomicAdd(p.flags + j, 0) == 0) __nanosleep(64);
+                    __threadfence();
+                }
+                epi_bar();
             }
             if (p.vec && !(p.dbg & 8)) {
                 // TMEM -> registers -> swizzled SMEM staging -> TMA bulk store (full lines,

@@ -39,6 +39,10 @@ def main():
     t0 = t[:, 0].min()
     rel = (t - t0) / 1000.0
     print("M=%d N=%d K=%d choice=%s event=%.2fus" % (M, N, K, ch.as_dict(), e0.elapsed_time(e1) * 1e3))
+    if "--late" in sys.argv:
+        order = np.argsort(-rel[:, 6])[:12]
+        for c in order:
+            print("  cta %3d " % c + " ".join("%7.2f" % x for x in rel[c]))
     for i, nm in enumerate(PH):
         col = rel[:, i]
         col = col[t[:, i] > 0]
