@@ -23,19 +23,19 @@ namespace vx {
 
 static const Calib kCalib = {
     /*hbm_milli=*/3329822,   // 6543 GB/s measured copy bandwidth / 1.965 GHz
-    /*dsm_milli=*/3012,      // effective in-cluster reduce rate (fitted)
-    /*fixed_cluster=*/540,  // cluster launch + two cluster barriers (fitted)
-    /*skfix_milli=*/2090,   // stream-K partial write + read-back (fitted)
+    /*dsm_milli=*/3070,      // effective in-cluster reduce rate (fitted)
+    /*fixed_cluster=*/231,  // cluster launch + two cluster barriers (fitted)
+    /*skfix_milli=*/3396,   // stream-K partial write + read-back (fitted)
 };
 
 static const RungCalib kRungs[] = {
-    {"umma_128x64", 1080625, 31687, 8421, 6364},
-    {"umma_128x128", 1604274, 90452, 15160, 2127},
-    {"umma_128x256", 2973207, 159915, 15404, 500},
-    {"umma_swap_128x16", 1000639, 35786, 8004, 6133},
-    {"umma_swap_128x32", 1000639, 27018, 8005, 5698},
-    {"umma_swap_128x64", 1000602, 34658, 8006, 4920},
-    {"umma_swap_128x128", 2245181, 58716, 9467, 6839},
+    {"umma_128x64", 1000591, 25592, 8003, 3519},
+    {"umma_128x128", 1538816, 159919, 15190, 620},
+    {"umma_128x256", 2647738, 159919, 39565, 500},
+    {"umma_swap_128x16", 1000639, 34677, 8003, 4621},
+    {"umma_swap_128x32", 1000639, 27594, 8003, 5702},
+    {"umma_swap_128x64", 1000639, 39012, 133216, 6643},
+    {"umma_swap_128x128", 1572433, 94555, 111315, 2976},
     {"simt_32x32", 128000, 32000, 16000, 2000},
     {"simt_64x64", 128000, 32000, 16000, 2000},
     {"simt_128x64", 128000, 32000, 16000, 2000},
