@@ -320,7 +320,8 @@ def _streamk_cost(rung, batch, M, N, K, mt, nt, tm, tn, tiles, kb, in_b, out_b, 
     """Stream-K schedule (R19): G = min(resident CTAs, U) CTAs share the U = tiles x k-blocks
     work units evenly in one wave (Eq. 3 gives F = 1); each CTA's temporal loop is
     ceil(U/G) k-blocks (Eq. 2) touching at most ceil(units/kb)+1 tile segments, whose
-    epilogues overlap the loop except the last; a cut tile adds one partial write + read."""
+    epilogues overlap the loop except the last; a cut tile is completed by adding
+    ceil(kb/units) partials, each one fp32 tile written and read back."""
     bm, bn, bk = rung["bm"], rung["bn"], rung["bk"]
     hbm = calib["hbm_milli"]
     U = tiles * kb
@@ -333,7 +334,7 @@ def _streamk_cost(rung, batch, M, N, K, mt, nt, tm, tn, tiles, kb, in_b, out_b, 
     tl = max(l_smem, l_hbm)
     t_main = temporal_cost(tl, units, inner, 0)
     st = max(t_load(bm * bn * out_b, cal["epi_milli"]), t_load(out_b * batch * M * N, segs * hbm))
-    fix = t_load(2 * bm * bn * 4, calib["skfix_milli"])
+    fix = ceil_div(kb, units) * t_load(2 * bm * bn * 4, calib["skfix_milli"])
     cost = max(t_main, segs * st) + st + fix + cal["fixed"]
     return {"cost": cost, "tiles_m": tm, "tiles_n": tn, "tiles": tiles, "F": 1, "grid": G,
             "padded_work": batch * tm * bm * tn * bn}

@@ -23,19 +23,19 @@ namespace vx {
 
 static const Calib kCalib = {
     /*hbm_milli=*/3329822,   // 6543 GB/s measured copy bandwidth / 1.965 GHz
-    /*dsm_milli=*/3070,      // effective in-cluster reduce rate (fitted)
-    /*fixed_cluster=*/231,  // cluster launch + two cluster barriers (fitted)
-    /*skfix_milli=*/3396,   // stream-K partial write + read-back (fitted)
+    /*dsm_milli=*/2951,      // effective in-cluster reduce rate (fitted)
+    /*fixed_cluster=*/318,  // cluster launch + two cluster barriers (fitted)
+    /*skfix_milli=*/9132,   // stream-K partial write + read-back (fitted)
 };
 
 static const RungCalib kRungs[] = {
-    {"umma_128x64", 1000591, 25592, 8003, 3519},
-    {"umma_128x128", 1538816, 159919, 15190, 620},
-    {"umma_128x256", 2647738, 159919, 39565, 500},
-    {"umma_swap_128x16", 1000639, 34677, 8003, 4621},
-    {"umma_swap_128x32", 1000639, 27594, 8003, 5702},
-    {"umma_swap_128x64", 1000639, 39012, 133216, 6643},
-    {"umma_swap_128x128", 1572433, 94555, 111315, 2976},
+    {"umma_128x64", 1000367, 28093, 22870, 4155},
+    {"umma_128x128", 1514912, 159400, 55762, 947},
+    {"umma_128x256", 2617401, 159352, 79545, 500},
+    {"umma_swap_128x16", 1004645, 24381, 8077, 4641},
+    {"umma_swap_128x32", 1004920, 27569, 465684, 6010},
+    {"umma_swap_128x64", 1003882, 38422, 483764, 5124},
+    {"umma_swap_128x128", 1521459, 157707, 501652, 1962},
     {"simt_32x32", 128000, 32000, 16000, 2000},
     {"simt_64x64", 128000, 32000, 16000, 2000},
     {"simt_128x64", 128000, 32000, 16000, 2000},

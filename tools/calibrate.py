@@ -49,42 +49,53 @@ def measure(args):
     json.dump(out, open(args.out, "w"))
 
 
-# ---- float model (DESIGN.md 3.3 without ceilings) ------------------------------------------
+# ---- integer model (DESIGN.md 3.3 / R19, the library's arithmetic) --------------------------
+def _cd(a, b):
+    return -(-a // b)
+
+
 def model_us(sm, th, desc, g):
-    """th: per-rung dict mac,l2s,epi,fixed (bytes or MACs per cycle); g: hbm,dsm,fixed_cluster."""
+    """th: per-rung dict mac,l2s,epi,fixed (per-cycle rates); g: hbm,dsm,fixed_cluster,skfix.
+    Rates are rounded to the library's x1000 integers and every division is a ceiling, so
+    the fitted constants are judged by exactly the decisions vx_plan_select will make."""
     M, N, K, s = sm["M"], sm["N"], sm["K"], sm["split"]
     bm, bn, bk = sm["bm"], sm["bn"], 64
+    mac, l2s, epi = (int(round(th[k] * 1000)) for k in ("mac", "l2s", "epi"))
+    fixed = int(round(th["fixed"]))
+    hbm, dsm, skfix = (int(round(g[k] * 1000)) for k in ("hbm", "dsm", "skfix"))
+    fixed_cluster = int(round(g["fixed_cluster"]))
+    t = lambda nbytes, bw: _cd(nbytes * 1000, bw)
     swap = sm["family"] == 1
     mt, nt = (N, M) if swap else (M, N)
-    tm, tn = -(-mt // bm), -(-nt // bn)
+    tm, tn = _cd(mt, bm), _cd(nt, bn)
     tiles = tm * tn
-    kb = -(-K // bk)
-    trips = kb // max(s, 1)
-    W = tiles * max(s, 1)
-    slots = desc["max_active_clusters"][str(max(s, 1))] * max(s, 1)
-    F = -(-W // slots)
-    c = bm * bn * bk / th["mac"]
-    ls = (min(bm, mt) + min(bn, nt)) * bk * 2 / th["l2s"]
+    kb = _cd(K, bk)
+    c = t(bm * bn * bk, mac)
+    ls = t((min(bm, mt) + min(bn, nt)) * bk * 2, l2s)
     if s == 0:   # stream-K (R19)
         U = tiles * kb
         G = min(desc["max_active_clusters"]["1"], U)
-        units = -(-U // G)
-        segs = -(-units // kb) + 1
-        l = max(ls, 2 * K * (mt + nt) / (units * g["hbm"]))
+        units = _cd(U, G)
+        segs = _cd(units, kb) + 1
+        l = max(ls, t(2 * K * (mt + nt), units * hbm))
         tm_ = l + (units - 1) * max(l, c) + c
-        st = max(bm * bn * 2 / th["epi"], 2 * M * N / (segs * g["hbm"]))
-        cyc = max(tm_, segs * st) + st + 2 * bm * bn * 4 / g["skfix"] + th["fixed"]
+        st = max(t(bm * bn * 2, epi), t(2 * M * N, segs * hbm))
+        cyc = max(tm_, segs * st) + st + _cd(kb, units) * t(2 * bm * bn * 4, skfix) + fixed
         return cyc / (CLOCK_GHZ * 1e3)
-    l = max(ls, 2 * K * (mt + nt) / (F * trips * g["hbm"]))
-    st = max(bm * bn * 2 / (s * th["epi"]), 2 * M * N / (F * g["hbm"]))
+    trips = kb // s
+    W = tiles * s
+    slots = desc["max_active_clusters"][str(s)] * s
+    F = _cd(W, slots)
+    l = max(ls, t(2 * K * (mt + nt), F * trips * hbm))
+    st = max(t(bm * bn * 2, s * epi), t(2 * M * N, F * hbm))
     if s > 1:
-        st += (s - 1) * bm * bn * 4 / (s * g["dsm"])
+        st += t((s - 1) * bm * bn * 4, s * dsm)
     T = l + (trips - 1) * max(l, c) + c + st
     if s == 1:
         tmain = T - st
-        cyc = tmain + (F - 1) * max(tmain, st) + st + th["fixed"]
+        cyc = tmain + (F - 1) * max(tmain, st) + st + fixed
     else:
-        cyc = F * T + th["fixed"] + g["fixed_cluster"]
+        cyc = F * T + fixed + fixed_cluster
     return cyc / (CLOCK_GHZ * 1e3)
 
 
