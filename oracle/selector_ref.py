@@ -134,10 +134,11 @@ EPI_STAGING = 32768                              # epilogue: 4 warps x 2 x 4 KB 
 CLUSTER_MAX = 8                                  # portable cluster size
 
 # kernels that exist in the library (the "implemented" filter, R6):
-#   family 0: tcgen05 cta_group::1, A-tile on the UMMA-M axis   (BM=128; BN in {64,128,256})
+#   family 0: tcgen05, A-tile on the UMMA-M axis: cta_group::1 BM=128, BN in {64,128,256};
+#             cta_group::2 pairs BM=256, BN in {128,256}
 #   family 1: same kernel with A/B swapped (N on UMMA-M, M on UMMA-N; BN in {16,32,64,128})
 #   family 2: fp32 SIMT FFMA (BM, BN, TM, TN) in {(32,32,2,4),(64,64,4,4),(128,64,8,4)}
-IMPL_TC = {(0, 128, 64), (0, 128, 128), (0, 128, 256),
+IMPL_TC = {(0, 128, 64), (0, 128, 128), (0, 128, 256), (0, 256, 128), (0, 256, 256),
            (1, 128, 16), (1, 128, 32), (1, 128, 64), (1, 128, 128)}
 SIMT_TILES = ((32, 32, 2, 4), (64, 64, 4, 4), (128, 64, 8, 4))
 SIMT_BK = 16
@@ -199,17 +200,20 @@ def build_table(K: int, in_dtype: str, out_dtype: str, desc: dict) -> dict:
         for (bm, bn, bk, S, st) in l2:
             cg = 2 if bm == 256 else 1
             for swap in (0, 1):
-                if (swap, bm, bn) not in IMPL_TC or cg != 1 or st != 2:
+                if (swap, bm, bn) not in IMPL_TC or st != 2:
                     continue
-                stage_bytes = (bm + bn) * bk * in_b
+                if cg == 2 and swap:      # cta_group::2 pair rungs are non-swapped
+                    continue
+                stage_bytes = (bm // cg + bn // cg) * bk * in_b
                 splits = []
                 for s in SPLITS:
                     if kb % s != 0 or s * cg > CLUSTER_MAX:
                         continue
-                    if s > 1 and bm * (bn + 4) * 4 > S * stage_bytes:
+                    if s > 1 and (cg > 1 or bm * (bn + 4) * 4 > S * stage_bytes):
                         continue
                     splits.append(s)
-                splits.append(0)          # stream-K schedule over (tile, k-block) units (R19)
+                if cg == 1:
+                    splits.append(0)      # stream-K schedule over (tile, k-block) units (R19)
                 rungs.append({"family": swap, "cg": cg, "um": bm, "un": bn, "acc_stages": st,
                               "bm": bm, "bn": bn, "bk": bk, "stages": S, "swap": swap,
                               "splits": splits})
@@ -275,7 +279,7 @@ def rung_cost(rung: dict, s: int, batch: int, M: int, N: int, K: int,
         return _streamk_cost(rung, batch, M, N, K, mt, nt, tm, tn, tiles, kb, in_b, out_b,
                              desc, calib, cal)
     trips = kb // s                                   # sizeof(TemporalLoop) at CTA level (R8)
-    W = tiles * s                                     # sizeof(ParallelLoop) at grid level
+    W = tiles * s * rung["cg"]                        # sizeof(ParallelLoop) in CTAs
     if rung["family"] == 2:
         slots = simt_slots(rung, desc)
     else:
@@ -311,7 +315,7 @@ def rung_cost(rung: dict, s: int, batch: int, M: int, N: int, K: int,
     else:
         cost = level_cost(F, T) + cal["fixed"] + (calib["fixed_cluster"] if s > 1 else 0)
     return {"cost": cost, "tiles_m": tm, "tiles_n": tn, "tiles": tiles, "F": F,
-            "grid": W if s > 1 or rung["family"] == 2 else min(tiles, slots),
+            "grid": W if s > 1 or rung["family"] == 2 else min(W, slots),
             "padded_work": batch * tm * bm * tn * bn}
 
 

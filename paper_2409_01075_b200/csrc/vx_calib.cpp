@@ -32,6 +32,8 @@ static const RungCalib kRungs[] = {
     {"umma_128x64", 1000367, 28093, 22870, 4155},
     {"umma_128x128", 1514912, 159400, 55762, 947},
     {"umma_128x256", 2617401, 159352, 79545, 500},
+    {"umma_256x128", 4096000, 96000, 16000, 3000},
+    {"umma_256x256", 6000000, 160000, 16000, 3000},
     {"umma_swap_128x16", 1004645, 24381, 8077, 4641},
     {"umma_swap_128x32", 1004920, 27569, 465684, 6010},
     {"umma_swap_128x64", 1003882, 38422, 483764, 5124},

@@ -30,7 +30,9 @@ static const bool g_pdl = [] {                 // VX_PDL=0 disables programmatic
 
 // ---- instantiated kernels (the "implemented" filter of the strategy table, R6) -----------
 bool kernel_available(int family, int bm, int bn) {
-    if (family == kUmma) return bm == 128 && (bn == 64 || bn == 128 || bn == 256);
+    if (family == kUmma)
+        return (bm == 128 && (bn == 64 || bn == 128 || bn == 256)) ||
+               (bm == 256 && (bn == 128 || bn == 256));     // cta_group::2 pair rungs
     if (family == kUmmaSwap) return bm == 128 && (bn == 16 || bn == 32 || bn == 64 || bn == 128);
     if (family == kSimt) return (bm == 32 && bn == 32) || (bm == 64 && bn == 64) || (bm == 128 && bn == 64);
     return false;
@@ -47,7 +49,20 @@ static UmmaFn pick_mn(bool b_mn) {
                 : (UmmaFn)vx_umma_kernel<BN, false, false, false>;
 }
 
-static UmmaFn umma_fn(int family, int bn, bool b_mn) {
+template <int BN>
+static UmmaFn pick_pair(bool b_mn) {
+    return b_mn ? (UmmaFn)vx_umma_kernel<BN, false, false, true, true>
+                : (UmmaFn)vx_umma_kernel<BN, false, false, false, true>;
+}
+
+static UmmaFn umma_fn(int family, int bm, int bn, bool b_mn) {
+    if (family == kUmma && bm == 256) {
+        switch (bn) {
+        case 128: return pick_pair<128>(b_mn);
+        case 256: return pick_pair<256>(b_mn);
+        }
+        return nullptr;
+    }
     if (family == kUmma) {
         switch (bn) {
         case 64: return pick_mn<64, false>(b_mn);
@@ -75,8 +90,10 @@ static SimtFn simt_fn(int bm, int bn, int* threads) {
     return nullptr;
 }
 
-static int64_t umma_smem_bytes(int bn, int stages) {
-    return (int64_t)stages * (128 + bn) * kBkTc * 2 + kSmemReserve + kEpiStaging;
+// per-CTA dynamic shared memory: S stages of (128 A rows + this CTA's B rows) x 128 B
+static int64_t umma_smem_bytes(int bm, int bn, int stages) {
+    const int cg = bm == 256 ? 2 : 1;
+    return (int64_t)stages * (bm / cg + bn / cg) * kBkTc * 2 + kSmemReserve + kEpiStaging;
 }
 
 static vx_status cuda_fail(cudaError_t e, const char* what) {
@@ -190,9 +207,10 @@ vx_status launch(const vx_plan_s* p, const vx_choice& ch, int64_t batch, int64_t
     }
     const bool swap = r.swap != 0;
     const bool b_mn = p->bl == VX_B_KN;
-    UmmaFn fn = umma_fn(r.family, r.bn, b_mn);
+    const bool pair = r.cg == 2;
+    UmmaFn fn = umma_fn(r.family, r.bm, r.bn, b_mn);
     if (!fn) { set_error("no tcgen05 kernel for rung %d", r.rung_id); return VX_ERR_UNSUPPORTED; }
-    const int64_t smem = umma_smem_bytes(r.bn, r.stages);
+    const int64_t smem = umma_smem_bytes(r.bm, r.bn, r.stages);
     vx_status s = ensure_attr((const void*)fn, smem);
     if (s != VX_OK) return s;
 
@@ -204,7 +222,7 @@ vx_status launch(const vx_plan_s* p, const vx_choice& ch, int64_t batch, int64_t
     if (b_mn) {
         s = make_map(&mapB, B, p->in, N, K, batch, N, batch > 1 ? sB : K * N, 64, 64);
     } else {
-        const int b_box = swap ? 128 : r.bn;
+        const int b_box = swap ? 128 : (pair ? r.bn / 2 : r.bn);
         s = make_map(&mapB, B, p->in, K, N, batch, K, batch > 1 ? sB : N * K, 64, b_box);
     }
     if (s != VX_OK) return s;
@@ -233,7 +251,8 @@ vx_status launch(const vx_plan_s* p, const vx_choice& ch, int64_t batch, int64_t
     const uint32_t p_major = (swap && b_mn) ? 1u : 0u;   // P operand MN-major?
     const uint32_t q_major = (!swap && b_mn) ? 1u : 0u;  // Q operand MN-major?
     prm.idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (p_major << 15) | (q_major << 16) |
-                ((uint32_t)(r.bn >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+                ((uint32_t)(r.bn >> 3) << 17) | ((uint32_t)((pair ? 256 : 128) >> 4) << 24);
+    prm.pair = pair ? 1 : 0;
     prm.C = C;
     prm.ldc = N;
     prm.sC = batch > 1 ? sC : M * N;
@@ -259,9 +278,9 @@ vx_status launch(const vx_plan_s* p, const vx_choice& ch, int64_t batch, int64_t
     cfg.stream = st;
     cudaLaunchAttribute attr[2];
     unsigned na = 0;
-    if (ch.split > 1) {   // split-K cluster (split 0 = stream-K, no cluster)
+    if (ch.split > 1 || pair) {   // split-K cluster or CTA pair (split 0 = stream-K)
         attr[na].id = cudaLaunchAttributeClusterDimension;
-        attr[na].val.clusterDim.x = (unsigned)ch.split;
+        attr[na].val.clusterDim.x = (unsigned)(pair ? 2 : ch.split);
         attr[na].val.clusterDim.y = 1;
         attr[na].val.clusterDim.z = 1;
         ++na;
@@ -291,9 +310,9 @@ vx_status prepare_kernels(const vx_plan_s* p) {
     }
     for (const vx::Rung& r : p->rungs) {
         if (r.family == kSimt) continue;
-        UmmaFn fn = umma_fn(r.family, r.bn, p->bl == VX_B_KN);
+        UmmaFn fn = umma_fn(r.family, r.bm, r.bn, p->bl == VX_B_KN);
         if (!fn) continue;
-        vx_status s = ensure_attr((const void*)fn, umma_smem_bytes(r.bn, r.stages));
+        vx_status s = ensure_attr((const void*)fn, umma_smem_bytes(r.bm, r.bn, r.stages));
         if (s != VX_OK) return s;
     }
     return VX_OK;
@@ -370,7 +389,7 @@ vx_status vx_device_probe(int device, vx_device_desc* out) {
     int cur = 0;
     cudaGetDevice(&cur);
     cudaSetDevice(device);
-    UmmaFn fn = umma_fn(kUmma, 128, false);
+    UmmaFn fn = umma_fn(kUmma, 128, 128, false);
     const int64_t smem = (int64_t)out->smem_optin;
     vx_status s = ensure_attr((const void*)fn, smem);
     if (s != VX_OK) { cudaSetDevice(cur); return s; }

@@ -133,17 +133,18 @@ static vx_status build_rungs(vx_plan_s* p) {
             int cg = c.bm == 256 ? 2 : 1;
             for (int swap = 0; swap <= 1; ++swap) {
                 int fam = swap ? kUmmaSwap : kUmma;
-                if (cg != 1 || c.st != 2 || !kernel_available(fam, c.bm, c.bn)) continue;
-                int64_t stage = (int64_t)(c.bm + c.bn) * c.bk * in_b;
+                if (c.st != 2 || !kernel_available(fam, c.bm, c.bn)) continue;
+                if (cg == 2 && swap) continue;      // pair rungs are non-swapped
+                int64_t stage = (int64_t)(c.bm / cg + c.bn / cg) * c.bk * in_b;
                 Rung r{};
                 r.family = fam; r.cg = cg; r.um = c.bm; r.un = c.bn; r.acc_stages = c.st;
                 r.bm = c.bm; r.bn = c.bn; r.bk = c.bk; r.stages = c.S; r.swap = swap;
                 for (int s : {1, 2, 4, 8}) {
                     if (kb % s != 0 || s * cg > kClusterMax) continue;
-                    if (s > 1 && (int64_t)c.bm * (c.bn + 4) * 4 > c.S * stage) continue;
+                    if (s > 1 && (cg > 1 || (int64_t)c.bm * (c.bn + 4) * 4 > c.S * stage)) continue;
                     r.splits.push_back(s);
                 }
-                r.splits.push_back(0);  // stream-K over (tile, k-block) units (R19)
+                if (cg == 1) r.splits.push_back(0);  // stream-K over (tile, k-block) units (R19)
                 rungs.push_back(r);
             }
         }
@@ -224,7 +225,7 @@ static void rung_cost(const vx_plan_s* p, const Rung& r, int s, int64_t batch, i
         return;
     }
     const int64_t trips = kb / s;            // sizeof(TemporalLoop) at the CTA level (R8)
-    const int64_t W = tiles * s;             // sizeof(ParallelLoop) at the grid level
+    const int64_t W = tiles * s * r.cg;      // sizeof(ParallelLoop) in CTAs at the grid level
     int64_t slots;
     if (r.family == kSimt) {
         int64_t threads = (bm / r.um) * (bn / r.un);
@@ -271,8 +272,8 @@ static void rung_cost(const vx_plan_s* p, const Rung& r, int s, int64_t batch, i
     o->stages = r.stages;
     o->tiles_m = (int32_t)tm;
     o->tiles_n = (int32_t)tn;
-    o->grid = (int32_t)((s > 1 || r.family == kSimt) ? W : std::min(tiles, slots));
-    o->cluster = s;
+    o->grid = (int32_t)((s > 1 || r.family == kSimt) ? W : std::min(W, slots));
+    o->cluster = s * r.cg;
     o->reserved = 0;
     o->cost = cost;
 }

@@ -54,6 +54,7 @@ struct UmmaParams {
                                 // reduce, 4 skip split C store, 8 skip epilogue stores,
                                 // 32 skip stream-K fix-up (timing experiments only)
     int streamk;                // 1: stream-K schedule over (tile, k-block) units
+    int pair;                   // 1: cta_group::2 pair rung (cluster of 2, 256-row tiles)
     float* ws;                  // stream-K partial slots [gridDim.x][128][BN] fp32 (plan-owned)
     int* flags;                 // stream-K slot-ready flags [gridDim.x] (0 between launches)
 };
@@ -73,6 +74,11 @@ struct WorkIter {
             const long long U = (long long)p.num_tiles * p.kb_total;
             u = (long long)blockIdx.x * U / gridDim.x;
             u1 = (long long)(blockIdx.x + 1) * U / gridDim.x;
+        } else if (p.pair) {
+            tile = blockIdx.x >> 1;          // both CTAs of a pair walk the same tiles
+            step = gridDim.x >> 1;
+            ka = 0;
+            kn = p.kb_total;
         } else if (p.splits > 1) {
             tile = blockIdx.x / p.splits;
             step = p.num_tiles;
@@ -297,12 +303,17 @@ __device__ __forceinline__ void sk_reset(const UmmaParams& p, int c0, int c1) {
 }
 
 // SWAP: P = B, Q = A.  P_MN / Q_MN: that operand is MN-major in SMEM (B stored K x N).
-template <int BN, bool SWAP, bool P_MN, bool Q_MN>
+// PAIR: cta_group::2 rung -- a cluster of 2 CTAs computes a 256 x BN tile; each CTA loads
+// its 128 rows of A and BN/2 rows of B, the leader (rank 0) issues the 256-row MMAs, each
+// CTA's TMEM holds its 128 rows of the accumulator (non-swap, persistent schedule only).
+template <int BN, bool SWAP, bool P_MN, bool Q_MN, bool PAIR = false>
 __global__ void __launch_bounds__(kThreads, 1)
     vx_umma_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmQ,
                    const __grid_constant__ CUtensorMap tmC, const UmmaParams p) {
+    static_assert(!PAIR || !SWAP, "pair rungs are non-swapped");
     using Cfg = UmmaCfg<BN>;
-    constexpr int kP = Cfg::kPBytes, kQ = Cfg::kQBytes;
+    constexpr int kP = Cfg::kPBytes;
+    constexpr int kQ = PAIR ? Cfg::kQBytes / 2 : Cfg::kQBytes;   // this CTA's B rows
     extern __shared__ __align__(1024) uint8_t smem_raw[];
 
     const int warp = threadIdx.x >> 5;
@@ -332,14 +343,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(&tfull[i], 1);
-            ptx::mbar_init(&tempty[i], kEpiWarps);
+            ptx::mbar_init(&tempty[i], PAIR ? 2 * kEpiWarps : kEpiWarps);
         }
         ptx::fence_mbar_init();
     }
-    if (warp == 1) ptx::tmem_alloc<Cfg::kTmemCols>(tmem_holder);
+    if (warp == 1) {
+        if (PAIR) ptx::tmem_alloc_pair<Cfg::kTmemCols>(tmem_holder);
+        else ptx::tmem_alloc<Cfg::kTmemCols>(tmem_holder);
+    }
     ptx::tc_fence_before();
-    __syncthreads();
+    if (PAIR) ptx::cluster_sync();   // both CTAs' barriers initialised before any remote use
+    else __syncthreads();
     ptx::tc_fence_after();
+    const uint32_t prank = PAIR ? ptx::cluster_ctarank() : 0;   // 0 = pair leader
     const uint32_t tmem_base = *tmem_holder;
     if (threadIdx.x == 0) trace_at(p, 1);
     // everything above (barrier init, TMEM alloc, descriptor prefetch) overlaps the previous
@@ -363,9 +379,27 @@ __global__ void __launch_bounds__(kThreads, 1)
                 decode_tile(tile, p.tiles_p, p.tiles_q, b, tp, tq);
                 for (int kb = k0; kb < k0 + nk; ++kb) {
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
-                    ptx::mbar_arrive_expect_tx(&full[stage], kP + kQ);
                     uint8_t* dP = sP + stage * kP;
                     uint8_t* dQ = sQ + stage * kQ;
+                    if (PAIR) {
+                        // both halves complete on the leader's full barrier
+                        if (prank == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2 * (kP + kQ));
+                        ptx::tma_load_3d_pair(dP, &tmP, &full[stage], kb * 64,
+                                              tp * 256 + (int)prank * 128, b, pol);
+                        if (Q_MN) {
+#pragma unroll
+                            for (int a = 0; a < BN / 128; ++a)
+                                ptx::tma_load_3d_pair(dQ + a * 8192, &tmQ, &full[stage],
+                                                      tq * BN + (int)prank * (BN / 2) + a * 64,
+                                                      kb * 64, b, pol);
+                        } else {
+                            ptx::tma_load_3d_pair(dQ, &tmQ, &full[stage], kb * 64,
+                                                  tq * BN + (int)prank * (BN / 2), b, pol);
+                        }
+                        if (++stage == S) { stage = 0; phase ^= 1; }
+                        continue;
+                    }
+                    ptx::mbar_arrive_expect_tx(&full[stage], kP + kQ);
                     if (P_MN) {  // [64 K rows x 64 MN] atoms, 8 KB apart
 #pragma unroll
                         for (int a = 0; a < 2; ++a)
@@ -389,8 +423,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             trace_at(p, 2);
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            // ===== MMA issuer (single thread) =====
+        if (lane == 0 && prank == 0) {
+            // ===== MMA issuer (single thread; the pair leader for PAIR rungs) =====
             int stage = 0;
             uint32_t phase = 0;
             int it = 0;
@@ -415,12 +449,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                  : ptx::sdesc_k_sw128(aP + k * 32);
                         const uint64_t dq = Q_MN ? ptx::sdesc_mn_sw128(aQ + k * 2048, 8192)
                                                  : ptx::sdesc_k_sw128(aQ + k * 32);
-                        ptx::umma_f16(d_tmem, dp, dq, p.idesc, (i | k) != 0);
+                        if (PAIR) ptx::umma_f16_pair(d_tmem, dp, dq, p.idesc, (i | k) != 0);
+                        else ptx::umma_f16(d_tmem, dp, dq, p.idesc, (i | k) != 0);
                     }
-                    ptx::umma_commit(&empty[stage]);  // frees the stage when these MMAs finish
+                    // frees the stage (in both CTAs of a pair) when these MMAs finish
+                    if (PAIR) ptx::umma_commit_pair(&empty[stage], 3);
+                    else ptx::umma_commit(&empty[stage]);
                     if (++stage == S) { stage = 0; phase ^= 1; }
                 }
-                ptx::umma_commit(&tfull[acc]);        // accumulator ready for the epilogue
+                // accumulator ready for the epilogue (of both CTAs of a pair)
+                if (PAIR) ptx::umma_commit_pair(&tfull[acc], 3);
+                else ptx::umma_commit(&tfull[acc]);
             }
             trace_at(p, 4);
         }
@@ -433,6 +472,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int row = quarter * 32 + lane;  // accumulator lane = row of the P tile
         const uint32_t wbuf = ptx::smem_addr(sE) + (uint32_t)(warp - kEpiWarp0) * 4096u;
         bool pending = false;                  // a TMA store still reads this warp's buffer
+        // TMEM buffer release: pairs arrive on the leader's barrier (it issues the MMAs)
+        auto release_acc = [&](uint64_t* bar) {
+            if (PAIR) ptx::mbar_arrive_remote(ptx::mapa(ptx::smem_addr(bar), 0));
+            else ptx::mbar_arrive(bar);
+        };
         int it = 0;
         WorkIter wi(p, rank);
         int tile, k0, nk;
@@ -440,6 +484,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (; wi.next(p, tile, k0, nk); ++it) {
             int b, tp, tq;
             decode_tile(tile, p.tiles_p, p.tiles_q, b, tp, tq);
+            // first P-axis row of this CTA's accumulator rows (a pair splits 256 rows)
+            const int prow0 = PAIR ? tp * 256 + (int)prank * 128 : tp * 128;
             const int acc = it & 1;
             const uint32_t acc_phase = (it >> 1) & 1;
             ptx::mbar_wait(&tfull[acc], acc_phase);
@@ -467,7 +513,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 ptx::tc_fence_before();
                 __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+                if (lane == 0) release_acc(&tempty[acc]);
                 __threadfence();
                 epi_bar();
                 if (threadIdx.x == kEpiWarp0 * 32) {
@@ -533,7 +579,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         __syncwarp();
                         if (lane == 0) {
                             ptx::tma_store_3d(&tmC, sE + (wbuf - ptx::smem_addr(sE)),
-                                              tq * BN + k * CW, tp * 128 + quarter * 32, b);
+                                              tq * BN + k * CW, prow0 + quarter * 32, b);
                             ptx::bulk_commit();
                         }
                         pending = true;
@@ -569,7 +615,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         __syncwarp();
                         if (lane == 0) {
                             ptx::tma_store_3d(&tmC, sE + (wbuf - ptx::smem_addr(sE)),
-                                              tp * 128 + quarter * 32, tq * BN + c * W, b);
+                                              prow0 + quarter * 32, tq * BN + c * W, b);
                             ptx::bulk_commit();
                         }
                         pending = true;
@@ -577,11 +623,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 ptx::tc_fence_before();
                 __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+                if (lane == 0) release_acc(&tempty[acc]);
                 if (c_last >= c_first) sk_reset(p, c_first, c_last);
                 continue;
             }
-            const int pr = tp * 128 + row;  // global index on the P axis
+            const int pr = prow0 + row;  // global index on the P axis
             char* Cb = reinterpret_cast<char*>(p.C) +
                        (long long)b * p.sC * (p.out_kind == 2 ? 4 : 2);
 #pragma unroll 1
@@ -610,7 +656,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             ptx::tc_fence_before();
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+            if (lane == 0) release_acc(&tempty[acc]);
             if (c_last >= c_first) sk_reset(p, c_first, c_last);
         }
         if (lane == 0) ptx::bulk_wait<0>();   // TMA stores complete before the CTA retires
@@ -703,11 +749,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (threadIdx.x == kEpiWarp0 * 32) trace_at(p, 7);
     ptx::tc_fence_before();
-    __syncthreads();
+    if (PAIR) ptx::cluster_sync();   // no CTA of a pair retires while its peer may touch it
+    else __syncthreads();
     if (warp == 1) {
         __syncwarp();
         ptx::tc_fence_after();
-        ptx::tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+        if (PAIR) ptx::tmem_dealloc_pair<Cfg::kTmemCols>(tmem_base);
+        else ptx::tmem_dealloc<Cfg::kTmemCols>(tmem_base);
     }
 }
 

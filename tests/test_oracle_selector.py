@@ -94,11 +94,12 @@ def test_table_invariants(K):
         assert r["bm"] % r["um"] == 0 and r["bn"] % r["un"] == 0 and r["bk"] % S.UMMA_K == 0
         assert S.isa_compatible_f16((r["um"], r["un"], S.UMMA_K))
         # resources: SMEM stages fit, TMEM accumulators fit
-        foot = r["stages"] * (r["bm"] + r["bn"]) * r["bk"] * 2 + S.SMEM_RESERVE + S.EPI_STAGING
+        cg = r["cg"]                                   # per-CTA footprint (pairs split tiles)
+        foot = r["stages"] * (r["bm"] // cg + r["bn"] // cg) * r["bk"] * 2 + S.SMEM_RESERVE + S.EPI_STAGING
         assert foot <= DESC["smem_optin"] and r["stages"] >= 2
         assert r["acc_stages"] * r["bn"] <= DESC["tmem_cols"]
         # split-K slices are whole k-blocks
-        assert 1 in r["splits"] and 0 in r["splits"]        # 0 = stream-K (R19)
+        assert 1 in r["splits"] and (0 in r["splits"]) == (cg == 1)   # 0 = stream-K (R19)
         assert all(s == 0 or kb % s == 0 for s in r["splits"])
     # sample-free and deterministic: a pure function of (K, dtypes, descriptor)
     assert S.build_table(K, "bf16", "bf16", DESC) == t

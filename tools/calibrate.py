@@ -82,9 +82,10 @@ def model_us(sm, th, desc, g):
         st = max(t(bm * bn * 2, epi), t(2 * M * N, segs * hbm))
         cyc = max(tm_, segs * st) + st + _cd(kb, units) * t(2 * bm * bn * 4, skfix) + fixed
         return cyc / (CLOCK_GHZ * 1e3)
+    cg = 2 if bm == 256 else 1
     trips = kb // s
-    W = tiles * s
-    slots = desc["max_active_clusters"][str(s)] * s
+    W = tiles * s * cg
+    slots = desc["max_active_clusters"][str(s * cg)] * s * cg
     F = _cd(W, slots)
     l = max(ls, t(2 * K * (mt + nt), F * trips * hbm))
     st = max(t(bm * bn * 2, s * epi), t(2 * M * N, F * hbm))
@@ -106,6 +107,7 @@ def fit(args):
     desc = raw["desc"]
     S = raw["samples"]
     keys = sorted({("umma_swap" if x["family"] == 1 else "umma", x["bm"], x["bn"]) for x in S})
+    ini0 = json.load(open(args.init)) if args.init else None
     names = ["%s_%dx%d" % k for k in keys]
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     hbm = peaks["hbm_gbs"] / CLOCK_GHZ
@@ -117,6 +119,8 @@ def fit(args):
     if args.init:
         ini = json.load(open(args.init))
         for i, n in enumerate(names):
+            if n not in ini["rungs"]:
+                continue
             r = ini["rungs"][n]
             x0[4 * i:4 * i + 4] = [math.log(r["mac_milli"] / 1000), math.log(r["l2s_milli"] / 1000),
                                    math.log(r["epi_milli"] / 1000), math.log(max(r["fixed"], 1))]
