@@ -149,7 +149,7 @@ def fit(args):
         for sm in S:
             pred = model_us(sm, th[key_of(sm)], desc, g)
             e += (math.log(pred) - math.log(sm["us"])) ** 2
-        e /= len(S)
+        e = args.err_weight * e / len(S)
         # selection quality: log-regret of the model's pick per calibration shape
         r = 0.0
         for k, v in groups.items():
@@ -164,9 +164,35 @@ def fit(args):
     lo += [math.log(2), math.log(1), math.log(1)]
     hi += [math.log(64), math.log(8000), math.log(256)]
     x0 = [min(max(v, a), b) for v, a, b in zip(x0, lo, hi)]
-    res = minimize(loss, np.array(x0), method="Powell", bounds=list(zip(lo, hi)),
-                   options={"maxiter": 40000, "xtol": 1e-3, "ftol": 1e-6})
-    th, g = unpack(res.x)
+    if args.method == "powell":
+        res = minimize(loss, np.array(x0), method="Powell", bounds=list(zip(lo, hi)),
+                       options={"maxiter": 40000, "xtol": 1e-3, "ftol": 1e-6})
+        xb = list(res.x)
+    else:
+        # greedy coordinate search on multiplicative steps: the regret objective is
+        # piecewise constant, so move one log-parameter at a time while it helps
+        xb = list(x0)
+        fb = loss(np.array(xb))
+        steps = [math.log(f) for f in (2.0, 1.4, 1.15, 1.05)]
+        for sweep in range(args.sweeps):
+            improved = False
+            for i in range(len(xb)):
+                for st in steps:
+                    for sg in (1, -1):
+                        xt = list(xb)
+                        xt[i] = min(max(xt[i] + sg * st, lo[i]), hi[i])
+                        ft = loss(np.array(xt))
+                        if ft < fb - 1e-9:
+                            xb, fb, improved = xt, ft, True
+            print("sweep %d objective %.5f" % (sweep, fb), flush=True)
+            if not improved:
+                break
+
+        class R:
+            pass
+        res = R()
+        res.fun = fb
+    th, g = unpack(xb)
     print("rms log error %.3f" % math.sqrt(res.fun))
     # regret of the fitted model on the calibration grid
     groups = {}
@@ -200,6 +226,9 @@ def main():
     f.add_argument("raw")
     f.add_argument("--regret-weight", type=float, default=2.0)
     f.add_argument("--init", default=None, help="start from a calibration json")
+    f.add_argument("--method", default="coord", choices=["coord", "powell"])
+    f.add_argument("--sweeps", type=int, default=12)
+    f.add_argument("--err-weight", type=float, default=1.0)
     args = ap.parse_args()
     if args.cmd == "measure":
         measure(args)
