@@ -21,8 +21,10 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-CAL_M = (1, 8, 32, 64, 128, 200, 512, 1024, 2048, 4096, 8192)
-CAL_NK = ((1024, 1024), (4096, 1024), (2048, 4096), (8192, 4096), (6144, 2048))
+CAL_M = (1, 8, 32, 64, 128, 200, 384, 512, 768, 1024, 1536, 2048, 3072, 4096, 8192)
+# generic (N, K): powers of two and N with odd tile counts (13 / 21 / 42 tiles of 256)
+CAL_NK = ((1024, 1024), (4096, 1024), (2048, 4096), (8192, 4096), (6144, 2048),
+          (3328, 1536), (5376, 4096), (10752, 2048))
 CLOCK_GHZ = 1.965   # cycles of the model are SM cycles at the max clock
 
 
