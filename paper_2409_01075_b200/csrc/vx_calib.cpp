@@ -24,20 +24,20 @@ namespace vx {
 static const Calib kCalib = {
     /*hbm_milli=*/3329822,   // 6543 GB/s measured copy bandwidth / 1.965 GHz
     /*dsm_milli=*/3078,      // effective in-cluster reduce rate (fitted)
-    /*fixed_cluster=*/717,  // cluster launch + two cluster barriers (fitted)
-    /*skfix_milli=*/9132,   // stream-K partial write + read-back (fitted)
+    /*fixed_cluster=*/738,  // cluster launch + two cluster barriers (fitted)
+    /*skfix_milli=*/9589,   // stream-K partial write + read-back (fitted)
 };
 
 static const RungCalib kRungs[] = {
-    {"umma_128x64", 1000367, 39330, 8000, 5495},
-    {"umma_128x128", 1442773, 160000, 180744, 1153},
-    {"umma_128x256", 1923790, 160000, 512000, 500},
-    {"umma_256x128", 3140267, 160000, 13251, 2857},
-    {"umma_256x256", 4096000, 160000, 512000, 1470},
-    {"umma_swap_128x16", 1000000, 24381, 8000, 4641},
-    {"umma_swap_128x32", 1000000, 30195, 465684, 6626},
-    {"umma_swap_128x64", 1000000, 34850, 507952, 5380},
-    {"umma_swap_128x128", 1449009, 77259, 512000, 1791},
+    {"umma_128x64", 1000367, 39330, 8000, 6018},
+    {"umma_128x128", 1442773, 160000, 506083, 955},
+    {"umma_128x256", 1672861, 160000, 512000, 500},
+    {"umma_256x128", 3140267, 160000, 13914, 2857},
+    {"umma_256x256", 4096000, 160000, 512000, 500},
+    {"umma_swap_128x16", 1000000, 34133, 8000, 3553},
+    {"umma_swap_128x32", 1000000, 36759, 17712, 4733},
+    {"umma_swap_128x64", 1000000, 42426, 507952, 7173},
+    {"umma_swap_128x128", 1449009, 160000, 512000, 1881},
     {"simt_32x32", 128000, 32000, 16000, 2000},
     {"simt_64x64", 128000, 32000, 16000, 2000},
     {"simt_128x64", 128000, 32000, 16000, 2000},
