@@ -475,9 +475,35 @@ def run_sharded(args, rank, world, local, vx, stream, side, l2):
     t = allreduce_max([statistics.median(ts)], world)[0]
     ch = p.select(m)
     del g, arenas
-    return {"M": M, "N": N, "K": K, "rows_per_rank": m, "ms": t,
-            "tflops": flops(M, N, K) / (t * 1e-3) / 1e12, "rung": ch["rung_id"],
-            "split": ch["split"], "gather": False, "launches_per_sample": R}
+    out = {"M": M, "N": N, "K": K, "rows_per_rank": m, "ms": t,
+           "tflops": flops(M, N, K) / (t * 1e-3) / 1e12, "rung": ch["rung_id"],
+           "split": ch["split"], "gather": False, "launches_per_sample": R}
+    if world > 1:
+        # optional gathered C: GEMM of this rank's rows, then ONE NCCL
+        # all_gather_into_tensor of the row shards; timed separately (communication-bound)
+        from paper_2409_01075_b200.dist import gather_rows
+        A = synth.matrix((m, K), "bf16", "normal", seed=77 + rank, device=stream.device)
+        B = synth.matrix((N, K), "bf16", "normal", seed=78, scale=K ** -0.5, device=stream.device)
+        C = torch.empty((m, N), dtype=torch.bfloat16, device=stream.device)
+        sp = ctypes.c_void_p(stream.cuda_stream)
+        gts = []
+        for i in range(4):
+            barrier(world)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            p.gemm_ptr(1, m, N, K, A.data_ptr(), m * K, B.data_ptr(), N * K, C.data_ptr(), m * N, sp)
+            full = gather_rows(C, M)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            if i:
+                gts.append(e0.elapsed_time(e1))
+        tg = allreduce_max([statistics.median(gts)], world)[0]
+        out["gathered_ms"] = tg
+        out["gathered_tflops"] = flops(M, N, K) / (tg * 1e-3) / 1e12
+        out["gathered_bytes_per_rank"] = 2 * (M - m) * N
+        del A, B, C, full
+    return out
 
 
 def run_e2e(args, rank, world, local, vx, plans, pts, stream):

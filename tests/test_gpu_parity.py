@@ -231,3 +231,45 @@ def test_device_descriptor_matches_golden():
     g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "b200_desc.json")))
     for k in ("sm_count", "smem_optin", "max_active_clusters", "tmem_cols"):
         assert d[k] == g[k], k
+
+
+def test_host_staged_e2e_path():
+    """vx_gemm_host: pinned host A,B -> device -> GEMM -> host C, on one stream."""
+    vx = vxmod()
+    M, N, K = 100, 256, 192
+    p = vx.Plan(N, K, "bf16", "fp32", "nk")
+    A, B = synth.gemm_inputs(M, N, K, "bf16", "nk", kind="int", seed=8)
+    hA, hB = A.pin_memory(), B.pin_memory()
+    hC = torch.empty((M, N), dtype=torch.float32).pin_memory()
+    dA = torch.empty_like(A, device="cuda")
+    dB = torch.empty_like(B, device="cuda")
+    dC = torch.empty((M, N), dtype=torch.float32, device="cuda")
+    s = torch.cuda.current_stream()
+    p.gemm_host(1, M, N, K, hA.data_ptr(), hB.data_ptr(), hC.data_ptr(), dA.data_ptr(),
+                dB.data_ptr(), dC.data_ptr(), __import__("ctypes").c_void_p(s.cuda_stream))
+    s.synchronize()
+    assert np.array_equal(hC.double().numpy(), oracle.gemm(A, B, "nk"))
+
+
+def test_sharded_gemm_nccl_single_rank():
+    """dist.ShardedGemm on a 1-rank NCCL group: library GEMM + all_gather path on the GPU."""
+    import os
+    import socket
+    import torch.distributed as dist
+    from paper_2409_01075_b200.dist import ShardedGemm
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        M, N, K = 77, 512, 256
+        A, B = synth.gemm_inputs(M, N, K, "bf16", "nk", kind="int", seed=2)
+        sg = ShardedGemm(N, K, in_dtype="bf16", out_dtype="fp32", device=0)
+        C = sg.forward(A.cuda(), B.cuda(), gather=True)
+        torch.cuda.synchronize()
+        assert np.array_equal(C.double().cpu().numpy(), oracle.gemm(A, B, "nk"))
+    finally:
+        dist.destroy_process_group()
