@@ -212,8 +212,7 @@ def build_table(K: int, in_dtype: str, out_dtype: str, desc: dict) -> dict:
                     if s > 1 and (cg > 1 or bm * (bn + 4) * 4 > S * stage_bytes):
                         continue
                     splits.append(s)
-                if cg == 1:
-                    splits.append(0)      # stream-K schedule over (tile, k-block) units (R19)
+                splits.append(0)          # stream-K schedule over (tile, k-block) units (R19)
                 rungs.append({"family": swap, "cg": cg, "um": bm, "un": bn, "acc_stages": st,
                               "bm": bm, "bn": bn, "bk": bk, "stages": S, "swap": swap,
                               "splits": splits})
@@ -329,7 +328,8 @@ def _streamk_cost(rung, batch, M, N, K, mt, nt, tm, tn, tiles, kb, in_b, out_b, 
     bm, bn, bk = rung["bm"], rung["bn"], rung["bk"]
     hbm = calib["hbm_milli"]
     U = tiles * kb
-    G = min(desc["max_active_clusters"]["1"], U)
+    cg = rung["cg"]                                  # units go to CTAs, or to CTA pairs
+    G = min(desc["max_active_clusters"][str(cg)], U)
     units = ceil_div(U, G)
     segs = ceil_div(units, kb) + 1
     inner = t_load(bm * bn * bk, cal["mac_milli"])
@@ -340,7 +340,7 @@ def _streamk_cost(rung, batch, M, N, K, mt, nt, tm, tn, tiles, kb, in_b, out_b, 
     st = max(t_load(bm * bn * out_b, cal["epi_milli"]), t_load(out_b * batch * M * N, segs * hbm))
     fix = ceil_div(kb, units) * t_load(2 * bm * bn * 4, calib["skfix_milli"])
     cost = max(t_main, segs * st) + st + fix + cal["fixed"]
-    return {"cost": cost, "tiles_m": tm, "tiles_n": tn, "tiles": tiles, "F": 1, "grid": G,
+    return {"cost": cost, "tiles_m": tm, "tiles_n": tn, "tiles": tiles, "F": 1, "grid": G * cg,
             "padded_work": batch * tm * bm * tn * bn}
 
 

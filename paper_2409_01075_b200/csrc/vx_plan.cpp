@@ -144,7 +144,7 @@ static vx_status build_rungs(vx_plan_s* p) {
                     if (s > 1 && (cg > 1 || (int64_t)c.bm * (c.bn + 4) * 4 > c.S * stage)) continue;
                     r.splits.push_back(s);
                 }
-                if (cg == 1) r.splits.push_back(0);  // stream-K over (tile, k-block) units (R19)
+                r.splits.push_back(0);  // stream-K over (tile, k-block) units (R19)
                 rungs.push_back(r);
             }
         }
@@ -205,7 +205,8 @@ static void rung_cost(const vx_plan_s* p, const Rung& r, int s, int64_t batch, i
     if (s == 0) {
         // stream-K (R19): G resident CTAs share U = tiles x k-blocks units evenly; one wave
         const int64_t U = tiles * kb;
-        const int64_t G = std::min<int64_t>(d.max_active_clusters[0], U);
+        // work is split over resident CTAs, or CTA pairs for cta_group::2 rungs
+        const int64_t G = std::min<int64_t>(d.max_active_clusters[r.cg == 2 ? 1 : 0], U);
         const int64_t units = cdiv(U, G);                       // temporal loop per CTA
         const int64_t segs = cdiv(units, kb) + 1;               // tile segments per CTA (bound)
         const int64_t inner = t_move(bm * bn * bk, r.mac_milli);
@@ -219,8 +220,8 @@ static void rung_cost(const vx_plan_s* p, const Rung& r, int s, int64_t batch, i
         const int64_t fix = cdiv(kb, units) * t_move(2 * bm * bn * 4, cal.skfix_milli);
         o->rung_id = r.rung_id; o->split = 0; o->family = r.family; o->swap = r.swap;
         o->bm = r.bm; o->bn = r.bn; o->stages = r.stages;
-        o->tiles_m = (int32_t)tm; o->tiles_n = (int32_t)tn; o->grid = (int32_t)G;
-        o->cluster = 1; o->reserved = 0;
+        o->tiles_m = (int32_t)tm; o->tiles_n = (int32_t)tn; o->grid = (int32_t)(G * r.cg);
+        o->cluster = r.cg; o->reserved = 0;
         o->cost = std::max(tm_, segs * st) + st + fix + r.fixed;
         return;
     }

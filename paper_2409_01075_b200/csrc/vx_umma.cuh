@@ -71,9 +71,12 @@ struct WorkIter {
     int ka, kn;            // split K range
     __device__ __forceinline__ WorkIter(const UmmaParams& p, int rank) {
         if (p.streamk) {
+            // stream-K units are split over CTAs, or over CTA pairs for pair rungs
             const long long U = (long long)p.num_tiles * p.kb_total;
-            u = (long long)blockIdx.x * U / gridDim.x;
-            u1 = (long long)(blockIdx.x + 1) * U / gridDim.x;
+            const long long id = p.pair ? (blockIdx.x >> 1) : blockIdx.x;
+            const long long G = p.pair ? (gridDim.x >> 1) : gridDim.x;
+            u = id * U / G;
+            u1 = (id + 1) * U / G;
         } else if (p.pair) {
             tile = blockIdx.x >> 1;          // both CTAs of a pair walk the same tiles
             step = gridDim.x >> 1;
@@ -276,13 +279,18 @@ __device__ __forceinline__ void store_col_chunk(char* Cb, long long ldc, int col
 
 // stream-K: add the fp32 partials of CTAs c0..c1 (in that order) for accumulator row `row`,
 // columns col0 .. col0+W-1, into the W values held as fp32 bits in v
-template <int W>
+// stream-K slot / flag of contributor id j (a CTA, or CTA `rank` of pair j)
+template <bool PAIR>
+__device__ __forceinline__ int sk_slot(int j, uint32_t rank) { return PAIR ? 2 * j + (int)rank : j; }
+
+template <int W, bool PAIR = false>
 __device__ __forceinline__ void add_partials(uint32_t* v, const float* ws, int c0, int c1, int row,
-                                             int col0, int bn) {
+                                             int col0, int bn, uint32_t rank = 0) {
 #pragma unroll 1
     for (int j = c0; j <= c1; ++j) {
         // slot layout [col/4][row][4]: a warp's 32 rows read 512 contiguous bytes
-        const float* src = ws + (long long)j * 128 * bn + ((long long)(col0 / 4) * 128 + row) * 4;
+        const float* src = ws + (long long)sk_slot<PAIR>(j, rank) * 128 * bn +
+                           ((long long)(col0 / 4) * 128 + row) * 4;
 #pragma unroll
         for (int i = 0; i < W; i += 4) {
             const float4 t = __ldcg(reinterpret_cast<const float4*>(src + i * 128));
@@ -296,10 +304,11 @@ __device__ __forceinline__ void add_partials(uint32_t* v, const float* ws, int c
 
 // stream-K: every epilogue warp has consumed slots c0..c1 -> clear their flags for the next
 // launch (each slot is produced and consumed exactly once per launch)
-__device__ __forceinline__ void sk_reset(const UmmaParams& p, int c0, int c1) {
+template <bool PAIR>
+__device__ __forceinline__ void sk_reset(const UmmaParams& p, int c0, int c1, uint32_t rank) {
     epi_bar();
     if (threadIdx.x == kEpiWarp0 * 32)
-        for (int j = c0; j <= c1; ++j) p.flags[j] = 0;
+        for (int j = c0; j <= c1; ++j) p.flags[sk_slot<PAIR>(j, rank)] = 0;
 }
 
 // SWAP: P = B, Q = A.  P_MN / Q_MN: that operand is MN-major in SMEM (B stored K x N).
@@ -495,6 +504,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (split) break;  // split mode: the accumulator is read after the cluster barrier
             // ---- stream-K: a cut tile ----------------------------------------------------
             int c_first = 0, c_last = -1;          // CTAs whose partials this CTA adds
+            // stream-K ids: CTAs, or pairs (each CTA of a pair fixes up its own 128 rows)
+            const int sk_id = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+            const int sk_G = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
             if (p.streamk && k0 > 0 && !(p.dbg & 32)) {
                 // not the owner: park the fp32 partial in this CTA's slot and publish it
                 // slot layout [col/4][row][4] (coalesced across the warp's rows)
@@ -523,18 +535,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                 continue;
             }
             if (p.streamk && nk < p.kb_total && !(p.dbg & 32)) {
-                // owner of a cut tile: the rest of its K range sits in CTAs c+1 .. c_last
-                c_first = blockIdx.x + 1;
+                // owner of a cut tile: the rest of its K range sits in ids sk_id+1 .. c_last
+                c_first = sk_id + 1;
                 const long long last_unit = (long long)(tile + 1) * p.kb_total - 1;
-                c_last = blockIdx.x;
-                while (c_last + 1 < (int)gridDim.x && sk_first(c_last + 1, U, gridDim.x) <= last_unit)
-                    ++c_last;
+                c_last = sk_id;
+                while (c_last + 1 < sk_G && sk_first(c_last + 1, U, sk_G) <= last_unit) ++c_last;
                 // one thread acquires the contributors' flags (backing off between polls so
                 // the publishers' stores are not starved); the named barrier then orders
                 // every epilogue thread's partial reads after that acquire
                 if (threadIdx.x == kEpiWarp0 * 32) {
                     for (int j = c_first; j <= c_last; ++j)
-                        while (atomicAdd(p.flags + j, 0) == 0) __nanosleep(64);
+                        while (atomicAdd(p.flags + sk_slot<PAIR>(j, prank), 0) == 0) __nanosleep(64);
                     __threadfence();
                 }
                 epi_bar();
@@ -556,7 +567,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             uint32_t v[32];
                             ptx::tmem_ld32(taddr + k * CW, v);
                             ptx::tmem_wait_ld();
-                            add_partials<32>(v, p.ws, c_first, c_last, row, k * CW, BN);
+                            add_partials<32, PAIR>(v, p.ws, c_first, c_last, row, k * CW, BN, prank);
 #pragma unroll
                             for (int j = 0; j < 8; ++j)
                                 ptx::st_shared_v4(rowa + (((uint32_t)(j ^ (lane & 7))) << 4),
@@ -567,7 +578,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             ptx::tmem_ld32(taddr + k * CW + 32,
                                            *reinterpret_cast<uint32_t(*)[32]>(v + 32));
                             ptx::tmem_wait_ld();
-                            add_partials<64>(v, p.ws, c_first, c_last, row, k * CW, BN);
+                            add_partials<64, PAIR>(v, p.ws, c_first, c_last, row, k * CW, BN, prank);
                             uint32_t u[32];
                             pack_chunk<64>(reinterpret_cast<const float*>(v), u, p.out_kind);
 #pragma unroll
@@ -596,7 +607,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         if (BN >= 32) ptx::tmem_ld32(taddr + c * 32, v);
                         else ptx::tmem_ld16(taddr + c * 32, v);
                         ptx::tmem_wait_ld();
-                        add_partials<W>(v, p.ws, c_first, c_last, row, c * 32, BN);
+                        add_partials<W, PAIR>(v, p.ws, c_first, c_last, row, c * 32, BN, prank);
                         const float* f = reinterpret_cast<const float*>(v);
                         // staging tile [W m-rows][32 n] (row pitch 32*ob bytes), lane = n
                         if (ob == 4) {
@@ -624,7 +635,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) release_acc(&tempty[acc]);
-                if (c_last >= c_first) sk_reset(p, c_first, c_last);
+                if (c_last >= c_first) sk_reset<PAIR>(p, c_first, c_last, prank);
                 continue;
             }
             const int pr = prow0 + row;  // global index on the P axis
@@ -637,7 +648,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 else ptx::tmem_ld16(taddr + c * 32, v);
                 ptx::tmem_wait_ld();
                 constexpr int W = BN >= 32 ? 32 : BN;
-                add_partials<W>(v, p.ws, c_first, c_last, row, c * 32, BN);
+                add_partials<W, PAIR>(v, p.ws, c_first, c_last, row, c * 32, BN, prank);
                 const float* f = reinterpret_cast<const float*>(v);
                 if (p.dbg & 8) {
                     if (f[0] == 12345.f) store1(Cb, 0, f[1], p.out_kind);
@@ -657,7 +668,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) release_acc(&tempty[acc]);
-            if (c_last >= c_first) sk_reset(p, c_first, c_last);
+            if (c_last >= c_first) sk_reset<PAIR>(p, c_first, c_last, prank);
         }
         if (lane == 0) ptx::bulk_wait<0>();   // TMA stores complete before the CTA retires
     }

@@ -76,7 +76,7 @@ def model_us(sm, th, desc, g):
     ls = t((min(bm, mt) + min(bn, nt)) * bk * 2, l2s)
     if s == 0:   # stream-K (R19)
         U = tiles * kb
-        G = min(desc["max_active_clusters"]["1"], U)
+        G = min(desc["max_active_clusters"]["2" if bm == 256 else "1"], U)
         units = _cd(U, G)
         segs = _cd(units, kb) + 1
         l = max(ls, t(2 * K * (mt + nt), units * hbm))
