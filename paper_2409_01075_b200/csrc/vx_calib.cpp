@@ -29,15 +29,15 @@ static const Calib kCalib = {
 };
 
 static const RungCalib kRungs[] = {
-    {"umma_128x64", 1000367, 39330, 8000, 6018},
+    {"umma_128x64", 1000367, 46531, 8000, 6635},
     {"umma_128x128", 1442773, 160000, 506083, 955},
     {"umma_128x256", 1672861, 160000, 512000, 500},
-    {"umma_256x128", 3140267, 160000, 13914, 2857},
+    {"umma_256x128", 3140267, 160000, 20454, 2721},
     {"umma_256x256", 4096000, 160000, 512000, 500},
-    {"umma_swap_128x16", 1000000, 34133, 8000, 3553},
-    {"umma_swap_128x32", 1000000, 36759, 17712, 4733},
-    {"umma_swap_128x64", 1000000, 42426, 507952, 7173},
-    {"umma_swap_128x128", 1449009, 160000, 512000, 1881},
+    {"umma_swap_128x16", 1000000, 39253, 8000, 4290},
+    {"umma_swap_128x32", 1000000, 35009, 17712, 2940},
+    {"umma_swap_128x64", 1217391, 46467, 507952, 7173},
+    {"umma_swap_128x128", 1449009, 160000, 512000, 1975},
     {"simt_32x32", 128000, 32000, 16000, 2000},
     {"simt_64x64", 128000, 32000, 16000, 2000},
     {"simt_128x64", 128000, 32000, 16000, 2000},
