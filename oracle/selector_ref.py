@@ -344,12 +344,27 @@ def _streamk_cost(rung, batch, M, N, K, mt, nt, tm, tn, tiles, kb, in_b, out_b, 
             "padded_work": batch * tm * bm * tn * bn}
 
 
+SK_MAX_WAVES = 3
+
+
+def streamk_admissible(rung: dict, batch: int, M: int, N: int, desc: dict) -> bool:
+    """R19: stream-K competes only where the rung's data-parallel schedule needs at most
+    SK_MAX_WAVES waves, i.e. where wave quantization is what it removes."""
+    mt, nt = (N, M) if rung["swap"] else (M, N)
+    tiles = batch * ceil_div(mt, rung["bm"]) * ceil_div(nt, rung["bn"])
+    cg = rung["cg"]
+    slots = desc["max_active_clusters"][str(cg)] * cg
+    return tiles * cg <= SK_MAX_WAVES * slots
+
+
 def select(table: dict, batch: int, M: int, N: int, K: int, desc: dict, calib: dict) -> dict:
     """Eq. 1 argmin over (rung, split); key (cost, padded_work, rung_id, split) (R13)."""
     assert M >= 1 and N >= 1 and batch >= 1
     best = None
     for r in table["rungs"]:
         for s in r["splits"]:
+            if s == 0 and not streamk_admissible(r, batch, M, N, desc):
+                continue
             c = rung_cost(r, s, batch, M, N, K, table["in"], table["out"], desc, calib)
             key = (c["cost"], c["padded_work"], r["rung_id"], s)
             if best is None or key < best[0]:

@@ -189,6 +189,16 @@ static vx_status build_rungs(vx_plan_s* p) {
     return VX_OK;
 }
 
+// stream-K is admitted only where wave quantization is what it fixes: the data-parallel
+// schedule of the rung needs at most kSkMaxWaves waves (R19)
+constexpr int64_t kSkMaxWaves = 3;
+static bool sk_admissible(const vx_plan_s* p, const Rung& r, int64_t batch, int64_t M, int64_t N) {
+    const int64_t mt = r.swap ? N : M, nt = r.swap ? M : N;
+    const int64_t tiles = batch * cdiv(mt, r.bm) * cdiv(nt, r.bn);
+    const int64_t slots = (int64_t)p->desc.max_active_clusters[r.cg == 2 ? 1 : 0] * r.cg;
+    return tiles * r.cg <= kSkMaxWaves * slots;
+}
+
 // ---- runtime cost ----------------------------------------------------------
 static void rung_cost(const vx_plan_s* p, const Rung& r, int s, int64_t batch, int64_t M,
                       int64_t N, vx_choice* o) {
@@ -308,6 +318,7 @@ vx_status select_choice(const vx_plan_s* p, int64_t batch, int64_t M, int64_t N,
     vx_choice best{};
     for (const Rung& r : p->rungs)
         for (int s : r.splits) {
+            if (s == 0 && !sk_admissible(p, r, batch, M, N)) continue;
             vx_choice c;
             rung_cost(p, r, s, batch, M, N, &c);
             if (!have || std::make_tuple(c.cost, padded_work(c, batch), c.rung_id, c.split) <

@@ -110,6 +110,8 @@ def _brute_best(t, batch, M, N, K):
     allc = []
     for r in t["rungs"]:
         for s in r["splits"]:
+            if s == 0 and not S.streamk_admissible(r, batch, M, N, DESC):   # R19
+                continue
             c = S.rung_cost(r, s, batch, M, N, K, t["in"], t["out"], DESC, CAL)
             allc.append((c["cost"], c["padded_work"], r["rung_id"], s))
     return min(allc)
@@ -164,3 +166,16 @@ def test_cost_monotone_in_bytes_and_rates():
     c3 = S.rung_cost(r, 1, 1, 8192, 4096, 4096, "bf16", "bf16", DESC, cal2)["cost"]
     c4 = S.rung_cost(r, 1, 1, 8192, 4096, 4096, "bf16", "bf16", DESC, CAL)["cost"]
     assert c3 <= c4
+
+
+def test_streamk_only_for_few_waves():
+    """R19: stream-K is never chosen when the rung's data-parallel grid needs > 3 waves."""
+    t = S.build_table(4096, "bf16", "bf16", DESC)
+    for M in (1, 64, 512, 1024, 4096, 16384, 65536):
+        ch = S.select(t, 1, M, 11008, 4096, DESC, CAL)
+        if ch["split"] == 0:
+            r = t["rungs"][ch["rung_id"]]
+            assert S.streamk_admissible(r, 1, M, 11008, DESC)
+    big = [r for r in t["rungs"] if r["cg"] == 2][0]
+    assert not S.streamk_admissible(big, 1, 16384, 11008, DESC)
+    assert S.streamk_admissible(big, 1, 512, 11008, DESC)

@@ -74,7 +74,10 @@ def model_us(sm, th, desc, g):
     kb = _cd(K, bk)
     c = t(bm * bn * bk, mac)
     ls = t((min(bm, mt) + min(bn, nt)) * bk * 2, l2s)
-    if s == 0:   # stream-K (R19)
+    if s == 0:   # stream-K (R19), admitted only for <= 3 data-parallel waves
+        cgk = 2 if bm == 256 else 1
+        if tiles * cgk > 3 * desc["max_active_clusters"][str(cgk)] * cgk:
+            return float("inf")
         U = tiles * kb
         G = min(desc["max_active_clusters"]["2" if bm == 256 else "1"], U)
         units = _cd(U, G)
