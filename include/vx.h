@@ -53,7 +53,10 @@ typedef enum { VX_BF16 = 0, VX_FP16 = 1, VX_FP32 = 2 } vx_dtype;
 
 typedef enum {
     VX_B_KN = 0, /* B stored row-major K x N                          */
-    VX_B_NK = 1  /* B stored row-major N x K (its transpose: linear weight, K^T of QK^T) */
+    VX_B_NK = 1, /* B stored row-major N x K (its transpose: linear weight, K^T of QK^T) */
+    VX_B_PACKED = 2 /* B pre-packed by vx_pack_b into contiguous 64 x 64 K-major tiles,
+                       [batch][ceil(N/64)][ceil(K/64)][64][64] (zero padded): every TMA box
+                       is one 8-KB contiguous block (weights streamed at full DRAM rate) */
 } vx_blayout;
 
 typedef enum {
@@ -172,7 +175,19 @@ vx_status vx_gemm_host(vx_plan_t plan, int64_t batch, int64_t M, int64_t N, int6
                        const void* A, const void* B, void* C, void* dA, void* dB, void* dC,
                        void* stream);
 
-/* Number of kernel launches this thread has issued through the library (evidence for
+/* Elements (of the plan's input dtype) of a packed B for (batch, N, K): batch x
+ * ceil(N/64)*64 x ceil(K/64)*64.  0 on bad arguments. */
+int64_t vx_packed_b_elems(vx_plan_t plan, int64_t batch, int64_t N, int64_t K);
+
+/* Pack B (device, stored in layout `src_layout` = VX_B_KN or VX_B_NK, batch stride sB
+ * elements) into the VX_B_PACKED layout at Bp (device, vx_packed_b_elems elements, 16-B
+ * aligned).  One kernel launch on `stream`; the plan must have b_layout VX_B_PACKED and a
+ * 16-bit input dtype.  Packing is a one-time cost per weight (inference weights are
+ * constant); vx_gemm on a VX_B_PACKED plan then takes Bp as its B. */
+vx_status vx_pack_b(vx_plan_t plan, int64_t batch, int64_t N, int64_t K, vx_blayout src_layout,
+                    const void* B, int64_t sB, void* Bp, void* stream);
+
+/* Number of kernel launches this process has issued through the library (evidence for
  * bench.py's gpu_launches). */
 int64_t vx_launch_count(void);
 

@@ -18,9 +18,9 @@ __all__ = ["VxError", "Plan", "DeviceDesc", "Choice", "lib", "plan", "gemm", "ge
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libvx.so")
 
 VX_BF16, VX_FP16, VX_FP32 = 0, 1, 2
-VX_B_KN, VX_B_NK = 0, 1
+VX_B_KN, VX_B_NK, VX_B_PACKED = 0, 1, 2
 _DT = {"bf16": VX_BF16, "fp16": VX_FP16, "fp32": VX_FP32}
-_BL = {"kn": VX_B_KN, "nk": VX_B_NK}
+_BL = {"kn": VX_B_KN, "nk": VX_B_NK, "packed": VX_B_PACKED}
 
 
 class VxError(RuntimeError):
@@ -95,6 +95,10 @@ def _load():
                              ctypes.POINTER(Choice)]
     L.vx_gemm_host.argtypes = [P, i64, i64, i64, i64, vp, vp, vp, vp, vp, vp, vp]
     L.vx_launch_count.restype = i64
+    L.vx_packed_b_elems.restype = i64
+    L.vx_packed_b_elems.argtypes = [P, i64, i64, i64]
+    L.vx_pack_b.argtypes = [P, i64, i64, i64, ctypes.c_int, vp, i64, vp, vp]
+    L.vx_pack_b.restype = ctypes.c_int
     for f in ("vx_device_probe", "vx_plan", "vx_plan_ex", "vx_plan_destroy", "vx_plan_select",
               "vx_plan_cost", "vx_plan_dump", "vx_gemm", "vx_gemm_batched", "vx_gemm_ex",
               "vx_gemm_host"):
@@ -181,11 +185,27 @@ class Plan:
         return json.loads(buf.value.decode())
 
     # ---- runtime -------------------------------------------------------------------------
+    def pack_b(self, B, src_layout: str = "nk", stream=None):
+        """One-time repack of a weight B ([N,K] "nk" or [K,N] "kn", optionally batched) into
+        the VX_B_PACKED layout this plan reads; returns the packed (flat) tensor."""
+        import torch
+        if self.b_layout != "packed":
+            raise ValueError("plan b_layout must be 'packed'")
+        batch = 1 if B.dim() == 2 else B.shape[0]
+        n = _lib.vx_packed_b_elems(self._h, batch, self.N, self.K)
+        out = torch.empty(n, dtype=B.dtype, device=B.device)
+        _check(_lib.vx_pack_b(self._h, batch, self.N, self.K, _BL[src_layout], B.data_ptr(),
+                              self.N * self.K, out.data_ptr(), _stream_ptr(stream)), "vx_pack_b")
+        out.vx_batch = batch
+        return out
+
     def _shape(self, A, B):
         if A.dim() == 2:
             batch, M, K = 1, A.shape[0], A.shape[1]
         else:
             batch, M, K = A.shape
+        if self.b_layout == "packed":
+            return batch, M, self.N, K
         if self.b_layout == "nk":
             N = B.shape[-2]
             if B.shape[-1] != K:

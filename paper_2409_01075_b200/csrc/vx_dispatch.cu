@@ -164,6 +164,49 @@ static vx_status make_map(CUtensorMap* map, const void* base, vx_dtype dt, int64
     return VX_OK;
 }
 
+// 5-D map over a VX_B_PACKED B: {64 k, 64 rows, k-block, row-block, batch}; one box = one
+// contiguous 8-KB 64 x 64 tile; OOB in any dimension (row / k / batch tails) reads zeros.
+static vx_status make_packed_map(CUtensorMap* map, const void* base, vx_dtype dt, int64_t N,
+                                 int64_t K, int64_t batch) {
+    EncodeTiledFn enc = encode_fn();
+    if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return VX_ERR_CUDA; }
+    const int64_t kb = (K + 63) / 64, rb = (N + 63) / 64;
+    cuuint64_t dims[5] = {64, 64, (cuuint64_t)kb, (cuuint64_t)rb, (cuuint64_t)batch};
+    cuuint64_t strides[4] = {128, 8192, (cuuint64_t)(8192 * kb), (cuuint64_t)(8192 * kb * rb)};
+    cuuint32_t box[5] = {64, 64, 1, 1, 1};
+    cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    CUresult r = enc(map, dt == VX_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                     5, const_cast<void*>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) { set_error("packed cuTensorMapEncodeTiled failed (%d)", (int)r); return VX_ERR_CUDA; }
+    return VX_OK;
+}
+
+// pack B (NK or KN storage) into [batch][rb][kb][64][64]: one thread per 8-element chunk
+__global__ void vx_pack_b_kernel(const uint16_t* __restrict__ B, uint16_t* __restrict__ out,
+                                 long long N, long long K, long long sB, int b_kn, long long rb,
+                                 long long kb, long long total_chunks) {
+    for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < total_chunks;
+         c += (long long)gridDim.x * blockDim.x) {
+        const long long j8 = c & 7, i = (c >> 3) & 63, t = c >> 9;   // chunk, row, tile
+        const long long kbi = t % kb, rbi = (t / kb) % rb, b = t / (kb * rb);
+        const long long n = rbi * 64 + i, k0 = kbi * 64 + j8 * 8;
+        uint16_t v[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const long long k = k0 + e;
+            v[e] = (n < N && k < K) ? (b_kn ? B[b * sB + k * N + n] : B[b * sB + n * K + k]) : 0;
+        }
+        uint4 u;
+        u.x = v[0] | ((uint32_t)v[1] << 16);
+        u.y = v[2] | ((uint32_t)v[3] << 16);
+        u.z = v[4] | ((uint32_t)v[5] << 16);
+        u.w = v[6] | ((uint32_t)v[7] << 16);
+        reinterpret_cast<uint4*>(out)[c] = u;
+    }
+}
+
 static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // stream-K workspace: one partial slot (128 x 256 fp32) + one flag per SM, allocated once
@@ -219,7 +262,9 @@ vx_status launch(const vx_plan_s* p, const vx_choice& ch, int64_t batch, int64_t
     const int a_box = swap ? r.bn : 128;  // A is P (box 128 rows) or Q (box BN rows)
     s = make_map(&mapA, A, p->in, K, M, batch, K, batch > 1 ? sA : M * K, 64, a_box);
     if (s != VX_OK) return s;
-    if (b_mn) {
+    if (p->bl == VX_B_PACKED) {
+        s = make_packed_map(&mapB, B, p->in, N, K, batch);
+    } else if (b_mn) {
         s = make_map(&mapB, B, p->in, N, K, batch, N, batch > 1 ? sB : K * N, 64, 64);
     } else {
         const int b_box = swap ? 128 : (pair ? r.bn / 2 : r.bn);
@@ -253,6 +298,7 @@ vx_status launch(const vx_plan_s* p, const vx_choice& ch, int64_t batch, int64_t
     prm.idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (p_major << 15) | (q_major << 16) |
                 ((uint32_t)(r.bn >> 3) << 17) | ((uint32_t)((pair ? 256 : 128) >> 4) << 24);
     prm.pair = pair ? 1 : 0;
+    prm.bpack = p->bl == VX_B_PACKED ? 1 : 0;
     prm.C = C;
     prm.ldc = N;
     prm.sC = batch > 1 ? sC : M * N;
@@ -454,6 +500,30 @@ vx_status vx_gemm_host(vx_plan_t p, int64_t batch, int64_t M, int64_t N, int64_t
     if (s != VX_OK) return s;
     e = cudaMemcpyAsync(C, dC, c_bytes, cudaMemcpyDeviceToHost, st);
     if (e != cudaSuccess) return cuda_fail(e, "D2H copy");
+    return VX_OK;
+}
+
+int64_t vx_packed_b_elems(vx_plan_t p, int64_t batch, int64_t N, int64_t K) {
+    if (!p || batch < 1 || N < 1 || K < 1) return 0;
+    return batch * cdiv(N, 64) * 64 * cdiv(K, 64) * 64;
+}
+
+vx_status vx_pack_b(vx_plan_t p, int64_t batch, int64_t N, int64_t K, vx_blayout src,
+                    const void* B, int64_t sB, void* Bp, void* stream) {
+    if (!p || !B || !Bp || batch < 1 || N < 1 || K < 1) { set_error("bad arguments"); return VX_ERR_INVALID; }
+    if (p->bl != VX_B_PACKED || p->in == VX_FP32) { set_error("plan is not a 16-bit VX_B_PACKED plan"); return VX_ERR_UNSUPPORTED; }
+    if (src != VX_B_KN && src != VX_B_NK) { set_error("source layout must be KN or NK"); return VX_ERR_INVALID; }
+    if (N != p->N || K != p->K) { set_error("N/K do not match the plan"); return VX_ERR_INVALID; }
+    if (!aligned16(Bp)) { set_error("packed buffer must be 16-byte aligned"); return VX_ERR_ALIGN; }
+    const int64_t rb = cdiv(N, 64), kb = cdiv(K, 64);
+    const int64_t chunks = batch * rb * kb * 512;
+    const int64_t sBe = batch > 1 ? sB : N * K;
+    vx_pack_b_kernel<<<(unsigned)std::min<int64_t>(cdiv(chunks, 256), 148 * 16), 256, 0,
+                       reinterpret_cast<cudaStream_t>(stream)>>>(
+        (const uint16_t*)B, (uint16_t*)Bp, N, K, sBe, src == VX_B_KN, rb, kb, chunks);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "pack launch");
+    g_launches.fetch_add(1, std::memory_order_relaxed);
     return VX_OK;
 }
 

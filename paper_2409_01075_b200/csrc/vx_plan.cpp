@@ -370,10 +370,13 @@ vx_status vx_plan_ex(int64_t N, int64_t K, vx_dtype in, vx_dtype out, vx_blayout
     if (!desc || !plan) { set_error("NULL argument"); return VX_ERR_INVALID; }
     *plan = nullptr;
     if (N < 0 || K <= 0) { set_error("need N >= 0 (0 = dynamic) and K > 0"); return VX_ERR_INVALID; }
-    if ((int)in < 0 || (int)in > 2 || (int)out < 0 || (int)out > 2 || ((int)bl != 0 && (int)bl != 1)) {
+    if ((int)in < 0 || (int)in > 2 || (int)out < 0 || (int)out > 2 || (int)bl < 0 || (int)bl > 2) {
         set_error("bad dtype or layout enum"); return VX_ERR_INVALID;
     }
     if (in == VX_FP32 && out != VX_FP32) { set_error("fp32 inputs need fp32 output"); return VX_ERR_UNSUPPORTED; }
+    if (bl == VX_B_PACKED && (in == VX_FP32 || N == 0)) {
+        set_error("VX_B_PACKED needs 16-bit inputs and a static N"); return VX_ERR_UNSUPPORTED;
+    }
     if (in != VX_FP32 && (K % 8 != 0 || (bl == VX_B_KN && N > 0 && N % 8 != 0))) {
         set_error("16-bit inputs need K %% 8 == 0 (and N %% 8 == 0 when B is K x N): TMA 16-byte strides");
         return VX_ERR_ALIGN;
@@ -433,7 +436,7 @@ vx_status vx_plan_dump(vx_plan_t p, char* buf, size_t cap, size_t* need) {
              "\"levels\":{\"l0\":%lld,\"l1\":%lld,\"l2\":%lld,\"l3\":%lld},"
              "\"calib\":{\"hbm_milli\":%lld,\"dsm_milli\":%lld,\"fixed_cluster\":%lld,\"skfix_milli\":%lld},\"rungs\":[",
              VX_ABI_VERSION, (long long)p->N, (long long)p->K, dt_name(p->in), dt_name(p->out),
-             p->bl == VX_B_KN ? "kn" : "nk", (long long)p->counts.l0, (long long)p->counts.l1,
+             p->bl == VX_B_KN ? "kn" : p->bl == VX_B_NK ? "nk" : "packed", (long long)p->counts.l0, (long long)p->counts.l1,
              (long long)p->counts.l2, (long long)p->counts.l3, (long long)c.hbm_milli,
              (long long)c.dsm_milli, (long long)c.fixed_cluster, (long long)c.skfix_milli);
     s += tmp;

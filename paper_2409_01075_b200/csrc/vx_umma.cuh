@@ -55,6 +55,7 @@ struct UmmaParams {
                                 // 32 skip stream-K fix-up (timing experiments only)
     int streamk;                // 1: stream-K schedule over (tile, k-block) units
     int pair;                   // 1: cta_group::2 pair rung (cluster of 2, 256-row tiles)
+    int bpack;                  // 1: B is VX_B_PACKED (5-D map of 64 x 64 contiguous tiles)
     float* ws;                  // stream-K partial slots [gridDim.x][128][BN] fp32 (plan-owned)
     int* flags;                 // stream-K slot-ready flags [gridDim.x] (0 between launches)
 };
@@ -395,7 +396,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                         if (prank == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2 * (kP + kQ));
                         ptx::tma_load_3d_pair(dP, &tmP, &full[stage], kb * 64,
                                               tp * 256 + (int)prank * 128, b, pol);
-                        if (Q_MN) {
+                        if (p.bpack) {             // this CTA's BN/2 rows = BN/128 packed tiles
+                            const int r0 = (tq * BN + (int)prank * (BN / 2)) / 64;
+#pragma unroll
+                            for (int a = 0; a < BN / 128; ++a)
+                                ptx::tma_load_5d_pair(dQ + a * 8192, &tmQ, &full[stage], 0, 0, kb,
+                                                      r0 + a, b, pol);
+                        } else if (Q_MN) {
 #pragma unroll
                             for (int a = 0; a < BN / 128; ++a)
                                 ptx::tma_load_3d_pair(dQ + a * 8192, &tmQ, &full[stage],
@@ -409,6 +416,24 @@ __global__ void __launch_bounds__(kThreads, 1)
                         continue;
                     }
                     ptx::mbar_arrive_expect_tx(&full[stage], kP + kQ);
+                    if (p.bpack) {
+                        // B pre-packed: every 64-row block of the B tile is one 8-KB box
+                        if (SWAP) {
+#pragma unroll
+                            for (int a = 0; a < 2; ++a)
+                                ptx::tma_load_5d(dP + a * 8192, &tmP, &full[stage], 0, 0, kb,
+                                                 tp * 2 + a, b, pol);
+                            ptx::tma_load_3d(dQ, &tmQ, &full[stage], kb * 64, tq * BN, b, pol);
+                        } else {
+                            ptx::tma_load_3d(dP, &tmP, &full[stage], kb * 64, tp * 128, b, pol);
+#pragma unroll
+                            for (int a = 0; a < BN / 64; ++a)
+                                ptx::tma_load_5d(dQ + a * 8192, &tmQ, &full[stage], 0, 0, kb,
+                                                 tq * (BN / 64) + a, b, pol);
+                        }
+                        if (++stage == S) { stage = 0; phase ^= 1; }
+                        continue;
+                    }
                     if (P_MN) {  // [64 K rows x 64 MN] atoms, 8 KB apart
 #pragma unroll
                         for (int a = 0; a < 2; ++a)

@@ -273,3 +273,21 @@ def test_sharded_gemm_nccl_single_rank():
         assert np.array_equal(C.double().cpu().numpy(), oracle.gemm(A, B, "nk"))
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("src", ["nk", "kn"])
+def test_packed_weights_every_rung_integer_exact(src):
+    """VX_B_PACKED: vx_pack_b repacks B into 64x64 contiguous tiles; every rung x schedule
+    reading the packed weight equals the oracle on integer inputs (N, K tails included)."""
+    vx = vxmod()
+    N, K = 392, 520                       # N and K not multiples of 64: zero-padded tiles
+    p = vx.Plan(N, K, "bf16", "fp32", "packed")
+    for M in (1, 130, 300):
+        A, B = synth.gemm_inputs(M, N, K, "bf16", src, kind="int", seed=40 + M)
+        want = oracle.gemm(A, B, src)
+        Bp = p.pack_b(B.cuda(), src)
+        for r in p.dump()["rungs"]:
+            for s in r["splits"]:
+                C, ch = p.gemm(A.cuda(), Bp, force=(r["rung_id"], s), want_choice=True)
+                torch.cuda.synchronize()
+                assert np.array_equal(C.cpu().double().numpy(), want), (src, M, r["rung_id"], s)
