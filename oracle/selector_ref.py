@@ -142,7 +142,11 @@ IMPL_TC = {(0, 128, 64), (0, 128, 128), (0, 128, 256), (0, 256, 128), (0, 256, 2
            (1, 128, 16), (1, 128, 32), (1, 128, 64), (1, 128, 128)}
 SIMT_TILES = ((32, 32, 2, 4), (64, 64, 4, 4), (128, 64, 8, 4))
 SIMT_BK = 16
-FAMILY_NAMES = {0: "umma", 1: "umma_swap", 2: "simt"}
+FAMILY_NAMES = {0: "umma", 1: "umma_swap", 2: "simt", 3: "gemv"}
+GEMV_MT = (1, 2, 4, 8)         # adaptive backend (R20): CUDA-core rungs for M <= MT
+GEMV_COLS = 32                 # 8 warps x 4 columns per CTA
+GEMV_BK = 256                  # k per warp iteration
+GEMV_OCC = 4                   # resident CTAs per SM assumed by the cost model
 
 
 def isa_compatible_f16(c) -> bool:
@@ -158,7 +162,7 @@ def isa_compatible_f16(c) -> bool:
     return False
 
 
-def build_table(K: int, in_dtype: str, out_dtype: str, desc: dict) -> dict:
+def build_table(K: int, in_dtype: str, out_dtype: str, desc: dict, b_layout: str = "nk") -> dict:
     """Alg. 2 bottom-up over the sm_100a levels; returns {'levels': counts, 'rungs': [...]}.
 
     L0 instruction tile, L1 TMEM accumulator tile, L2 CTA/SMEM tile, L3 grid schedule.
@@ -216,6 +220,12 @@ def build_table(K: int, in_dtype: str, out_dtype: str, desc: dict) -> dict:
                 rungs.append({"family": swap, "cg": cg, "um": bm, "un": bn, "acc_stages": st,
                               "bm": bm, "bn": bn, "bk": bk, "stages": S, "swap": swap,
                               "splits": splits})
+        # adaptive backend (R20): CUDA-core rungs join the same argmin
+        if b_layout != "packed":
+            for mt in GEMV_MT:
+                rungs.append({"family": 3, "cg": 1, "um": 1, "un": 1, "acc_stages": 1,
+                              "bm": mt, "bn": GEMV_COLS, "bk": GEMV_BK, "stages": 1, "swap": 0,
+                              "splits": [1]})
         counts = {"l0": len(l0), "l1": len(l1), "l2": len(l2), "l3": len(rungs)}
     elif in_dtype == "fp32":
         # CUDA-core mode: L0 = FFMA thread tiles, L2 = CTA tiles
@@ -269,6 +279,8 @@ def rung_cost(rung: dict, s: int, batch: int, M: int, N: int, K: int,
     cal = _calib_for(rung, calib)
     hbm = calib["hbm_milli"]
     bm, bn, bk = rung["bm"], rung["bn"], rung["bk"]
+    if rung["family"] == 3:
+        return _gemv_cost(rung, batch, M, N, K, in_b, out_b, desc, calib, cal)
     # padding only at the outermost (grid) level (Fig. padding)
     mt, nt = (N, M) if rung["swap"] else (M, N)
     tm, tn = ceil_div(mt, bm), ceil_div(nt, bn)
@@ -318,6 +330,24 @@ def rung_cost(rung: dict, s: int, batch: int, M: int, N: int, K: int,
             "padded_work": batch * tm * bm * tn * bn}
 
 
+def _gemv_cost(rung, batch, M, N, K, in_b, out_b, desc, calib, cal):
+    """CUDA-core GEMV rung (R20): a CTA holds MT rows x 32 columns and walks K in steps of
+    256; GEMV_OCC CTAs per SM; Eqs. 2-4 as for the other rungs."""
+    bm, bn, bk = rung["bm"], rung["bn"], rung["bk"]
+    hbm = calib["hbm_milli"]
+    tiles = batch * ceil_div(N, bn)
+    F = parallel_factor(tiles, desc["sm_count"] * GEMV_OCC)        # Eq. 3
+    trips = ceil_div(K, bk)
+    inner = t_load(bm * bn * bk, cal["mac_milli"])
+    l_smem = t_load(bn * bk * in_b + bm * bk * in_b, cal["l2s_milli"])
+    l_hbm = t_load(in_b * batch * K * (N + M), F * trips * hbm)
+    tl = max(l_smem, l_hbm)
+    ts = max(t_load(bm * bn * out_b, cal["epi_milli"]), t_load(out_b * batch * M * N, F * hbm))
+    cost = level_cost(F, temporal_cost(tl, trips, inner, ts)) + cal["fixed"]   # Eqs. 2, 4
+    return {"cost": cost, "tiles_m": 1, "tiles_n": ceil_div(N, bn), "tiles": tiles, "F": F,
+            "grid": tiles, "padded_work": batch * bm * ceil_div(N, bn) * bn}
+
+
 def _streamk_cost(rung, batch, M, N, K, mt, nt, tm, tn, tiles, kb, in_b, out_b, desc, calib,
                   cal):
     """Stream-K schedule (R19): G = min(resident CTAs, U) CTAs share the U = tiles x k-blocks
@@ -364,6 +394,8 @@ def select(table: dict, batch: int, M: int, N: int, K: int, desc: dict, calib: d
     for r in table["rungs"]:
         for s in r["splits"]:
             if s == 0 and not streamk_admissible(r, batch, M, N, desc):
+                continue
+            if r["family"] == 3 and M > r["bm"]:      # GEMV rungs hold M <= MT rows (R20)
                 continue
             c = rung_cost(r, s, batch, M, N, K, table["in"], table["out"], desc, calib)
             key = (c["cost"], c["padded_work"], r["rung_id"], s)

@@ -17,7 +17,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libvx.so")
 SOURCES = ["vx_plan.cpp", "vx_calib.cpp", "vx_dispatch.cu"]
-HEADERS = ["vx_internal.h", "vx_ptx.cuh", "vx_umma.cuh", "vx_simt.cuh"]
+HEADERS = ["vx_internal.h", "vx_ptx.cuh", "vx_umma.cuh", "vx_simt.cuh", "vx_gemv.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -12,6 +12,7 @@
 #include <mutex>
 
 #include "vx_internal.h"
+#include "vx_gemv.cuh"
 #include "vx_simt.cuh"
 #include "vx_umma.cuh"
 
@@ -35,6 +36,7 @@ bool kernel_available(int family, int bm, int bn) {
                (bm == 256 && (bn == 128 || bn == 256));     // cta_group::2 pair rungs
     if (family == kUmmaSwap) return bm == 128 && (bn == 16 || bn == 32 || bn == 64 || bn == 128);
     if (family == kSimt) return (bm == 32 && bn == 32) || (bm == 64 && bn == 64) || (bm == 128 && bn == 64);
+    if (family == kGemv) return (bm == 1 || bm == 2 || bm == 4 || bm == 8) && bn == kGemvCols;
     return false;
 }
 
@@ -245,6 +247,39 @@ vx_status launch(const vx_plan_s* p, const vx_choice& ch, int64_t batch, int64_t
                                                (int)N, (int)K, p->bl == VX_B_NK, sA, sB, sC, tm, tn);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_fail(e, "SIMT launch");
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        return VX_OK;
+    }
+    if (r.family == kGemv) {
+        using GemvFn = void (*)(const uint16_t*, const uint16_t*, void*, int, int, int, long long,
+                                long long, long long, int, int);
+        const bool kn = p->bl == VX_B_KN;
+        GemvFn fn = nullptr;
+        switch (r.bm) {
+        case 1: fn = kn ? vx_gemv_kernel<1, true> : vx_gemv_kernel<1, false>; break;
+        case 2: fn = kn ? vx_gemv_kernel<2, true> : vx_gemv_kernel<2, false>; break;
+        case 4: fn = kn ? vx_gemv_kernel<4, true> : vx_gemv_kernel<4, false>; break;
+        case 8: fn = kn ? vx_gemv_kernel<8, true> : vx_gemv_kernel<8, false>; break;
+        }
+        if (!fn || M > r.bm) { set_error("no GEMV kernel for rung %d / M=%lld", r.rung_id, (long long)M); return VX_ERR_UNSUPPORTED; }
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)cdiv(N, kGemvCols), (unsigned)batch, 1);
+        cfg.blockDim = dim3(kGemvWarps * 32, 1, 1);
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        if (g_pdl) {
+            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+        }
+        const long long sCe = batch > 1 ? sC : M * N;
+        cudaError_t e = cudaLaunchKernelEx(&cfg, fn, (const uint16_t*)A, (const uint16_t*)B, C,
+                                           (int)M, (int)N, (int)K, (long long)(batch > 1 ? sA : M * K),
+                                           (long long)(batch > 1 ? sB : N * K), sCe,
+                                           p->in == VX_BF16 ? 0 : 1,
+                                           p->out == VX_BF16 ? 0 : p->out == VX_FP16 ? 1 : 2);
+        if (e != cudaSuccess) return cuda_fail(e, "GEMV launch");
         g_launches.fetch_add(1, std::memory_order_relaxed);
         return VX_OK;
     }

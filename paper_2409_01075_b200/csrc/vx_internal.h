@@ -14,7 +14,7 @@
 namespace vx {
 
 // Kernel families of the ladder's top level
-enum Family : int32_t { kUmma = 0, kUmmaSwap = 1, kSimt = 2 };
+enum Family : int32_t { kUmma = 0, kUmmaSwap = 1, kSimt = 2, kGemv = 3 };
 
 constexpr int kBkTc = 64;          // one 128-B swizzle row of 2-byte elements
 constexpr int kUmmaK = 16;         // kind::f16 instruction K
@@ -23,6 +23,9 @@ constexpr int kSmemReserve = 2048; // barriers + 1024-B alignment slack
 constexpr int kEpiStaging = 32768; // epilogue: 4 warps x 2 x 4 KB TMA-store staging tiles
 constexpr int kClusterMax = 8;     // portable cluster size
 constexpr int kSimtBk = 16;
+constexpr int kGemvBk = 256;        // k per warp iteration (32 lanes x 8 elements)
+constexpr int kGemvColsPerCta = 32; // 8 warps x 4 columns
+constexpr int kGemvOcc = 4;         // resident CTAs per SM assumed by the cost model (R20)
 
 // One rung = one full chain L0 -> L1 -> L2 -> L3 of the strategy table (Alg. 2 map).
 struct Rung {

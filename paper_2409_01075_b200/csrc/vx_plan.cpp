@@ -88,7 +88,9 @@ std::vector<C> sieve(const std::vector<C>& cands, const std::vector<P>& prev, Di
     return out;
 }
 
-const char* family_name(int f) { return f == kUmma ? "umma" : f == kUmmaSwap ? "umma_swap" : "simt"; }
+const char* family_name(int f) {
+    return f == kUmma ? "umma" : f == kUmmaSwap ? "umma_swap" : f == kSimt ? "simt" : "gemv";
+}
 
 }  // namespace
 
@@ -148,6 +150,17 @@ static vx_status build_rungs(vx_plan_s* p) {
                 rungs.push_back(r);
             }
         }
+        // adaptive backend (R20): CUDA-core GEMV-style rungs for tiny M (M <= MT), competing
+        // in the same argmin; not for pre-packed weights
+        if (p->bl != VX_B_PACKED)
+            for (int mt : {1, 2, 4, 8}) {
+                if (!kernel_available(kGemv, mt, kGemvColsPerCta)) continue;
+                Rung r{};
+                r.family = kGemv; r.cg = 1; r.um = 1; r.un = 1; r.acc_stages = 1;
+                r.bm = mt; r.bn = kGemvColsPerCta; r.bk = kGemvBk; r.stages = 1; r.swap = 0;
+                r.splits = {1};
+                rungs.push_back(r);
+            }
         p->counts = {(int64_t)l0.size(), (int64_t)l1.size(), (int64_t)l2.size(), (int64_t)rungs.size()};
     } else {
         // CUDA-core mode: L0 FFMA thread tiles, L2 CTA tiles (BK = 16)
@@ -212,6 +225,25 @@ static void rung_cost(const vx_plan_s* p, const Rung& r, int s, int64_t batch, i
     const int64_t tm = cdiv(mt, bm), tn = cdiv(nt, bn);
     const int64_t tiles = batch * tm * tn;
     const int64_t kb = cdiv(K, bk);
+    if (r.family == kGemv) {
+        // CUDA-core GEMV rung (R20): a CTA = MT rows x 32 columns; k-steps of 256
+        const int64_t tiles_g = batch * cdiv(N, bn);
+        const int64_t slots_g = (int64_t)d.sm_count * kGemvOcc;
+        const int64_t Fg = eq3(tiles_g, slots_g);
+        const int64_t trips_g = cdiv(K, bk);
+        const int64_t inner_g = t_move(bm * bn * bk, r.mac_milli);
+        const int64_t ls_g = t_move(bn * bk * in_b + bm * bk * in_b, r.l2s_milli);
+        const int64_t lh_g = t_move((int64_t)in_b * batch * K * (N + M), Fg * trips_g * cal.hbm_milli);
+        const int64_t tl_g = std::max(ls_g, lh_g);
+        const int64_t ts_g = std::max(t_move(bm * bn * out_b, r.epi_milli),
+                                      t_move((int64_t)out_b * batch * M * N, Fg * cal.hbm_milli));
+        o->rung_id = r.rung_id; o->split = 1; o->family = r.family; o->swap = 0;
+        o->bm = r.bm; o->bn = r.bn; o->stages = r.stages;
+        o->tiles_m = 1; o->tiles_n = (int32_t)cdiv(N, bn); o->grid = (int32_t)tiles_g;
+        o->cluster = 1; o->reserved = 0;
+        o->cost = Fg * eq2(tl_g, trips_g, inner_g, ts_g) + r.fixed;
+        return;
+    }
     if (s == 0) {
         // stream-K (R19): G resident CTAs share U = tiles x k-blocks units evenly; one wave
         const int64_t U = tiles * kb;
@@ -305,6 +337,10 @@ vx_status select_choice(const vx_plan_s* p, int64_t batch, int64_t M, int64_t N,
             set_error("split %d not admissible for rung %d", force_split, force_rung);
             return VX_ERR_INVALID;
         }
+        if (r.family == kGemv && M > r.bm) {
+            set_error("GEMV rung %d holds at most %d rows", force_rung, r.bm);
+            return VX_ERR_INVALID;
+        }
         rung_cost(p, r, force_split, batch, M, N, out);
         return VX_OK;
     }
@@ -319,6 +355,7 @@ vx_status select_choice(const vx_plan_s* p, int64_t batch, int64_t M, int64_t N,
     for (const Rung& r : p->rungs)
         for (int s : r.splits) {
             if (s == 0 && !sk_admissible(p, r, batch, M, N)) continue;
+            if (r.family == kGemv && M > r.bm) continue;   // GEMV rungs hold M <= MT rows
             vx_choice c;
             rung_cost(p, r, s, batch, M, N, &c);
             if (!have || std::make_tuple(c.cost, padded_work(c, batch), c.rung_id, c.split) <

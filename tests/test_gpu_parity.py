@@ -40,6 +40,11 @@ def _tol(ref, K, out):
     return base + rel * np.abs(ref)
 
 
+def _ok(r, M):
+    """(rung, M) is launchable: GEMV rungs (family 3, R20) hold at most MT = bm rows."""
+    return r["family"] != 3 or M <= r["bm"]
+
+
 def _run(p, A, B, force=None):
     C, ch = p.gemm(A.cuda(), B.cuda(), force=force, want_choice=True)
     torch.cuda.synchronize()
@@ -56,6 +61,8 @@ def test_every_rung_and_split_integer_exact(bl, out):
         A, B = synth.gemm_inputs(M, N, K, "bf16", bl, kind="int", seed=100 + M)
         want = _round_to(oracle.gemm(A, B, bl), out)
         for r in p.dump()["rungs"]:
+            if not _ok(r, M):
+                continue
             for s in r["splits"]:
                 got, ch = _run(p, A, B, force=(r["rung_id"], s))
                 assert ch["rung_id"] == r["rung_id"] and ch["split"] == s
@@ -70,6 +77,8 @@ def test_fp16_inputs_integer_exact():
         A, B = synth.gemm_inputs(M, N, K, "fp16", "nk", kind="int", seed=M)
         want = _round_to(oracle.gemm(A, B, "nk"), "fp16")
         for r in p.dump()["rungs"]:
+            if not _ok(r, M):
+                continue
             for s in r["splits"]:
                 got, _ = _run(p, A, B, force=(r["rung_id"], s))
                 assert np.array_equal(got, want), (M, r["rung_id"], s)
@@ -153,6 +162,8 @@ def test_pad_poisoning():
         want = oracle.gemm(A, B, "nk")
         Bd = B.cuda()
         for r in p.dump()["rungs"]:
+            if not _ok(r, M):
+                continue
             for s in r["splits"]:
                 Cbig.fill_(12345.0)
                 vx.lib.vx_gemm_ex(p.handle, 1, M, N, K, Abig.data_ptr(), M * K, Bd.data_ptr(),
@@ -174,6 +185,8 @@ def test_batched_attention_scores(d):
         got, ch = _run(p, Q, Kt)
         assert np.array_equal(got, want), (d, s, ch)
         for r in p.dump()["rungs"]:
+            if not _ok(r, s):
+                continue
             got, _ = _run(p, Q, Kt, force=(r["rung_id"], r["splits"][-1]))
             assert np.array_equal(got, want), (d, s, r)
 
@@ -202,6 +215,8 @@ def test_fp32_simt_path():
             A, B = synth.gemm_inputs(M, 64, 64, "fp32", bl, kind="normal", seed=M)
             ref = oracle.gemm(A, B, bl)
             for r in p.dump()["rungs"]:
+                if not _ok(r, M):
+                    continue
                 got, ch = _run(p, A, B, force=(r["rung_id"], 1))
                 assert np.abs(got - ref).max() <= 1e-5 * np.abs(ref).max(), (bl, M, r)
     # config 1 exactly: M=37, N=64, K=64 via the selector
@@ -287,7 +302,36 @@ def test_packed_weights_every_rung_integer_exact(src):
         want = oracle.gemm(A, B, src)
         Bp = p.pack_b(B.cuda(), src)
         for r in p.dump()["rungs"]:
+            if not _ok(r, M):
+                continue
             for s in r["splits"]:
                 C, ch = p.gemm(A.cuda(), Bp, force=(r["rung_id"], s), want_choice=True)
                 torch.cuda.synchronize()
                 assert np.array_equal(C.cpu().double().numpy(), want), (src, M, r["rung_id"], s)
+
+
+@pytest.mark.parametrize("bl", ["nk", "kn"])
+@pytest.mark.parametrize("out", ["fp32", "bf16", "fp16"])
+def test_gemv_rungs_tiny_m(bl, out):
+    """Adaptive backend (R20): the CUDA-core GEMV rungs for M <= MT, integer-exact, with N
+    and K tails, both B layouts and every output type; batched too."""
+    vx = vxmod()
+    N, K = 392, 520
+    p = vx.Plan(N, K, "bf16", out, bl)
+    rungs = [r for r in p.dump()["rungs"] if r["family"] == 3]
+    assert [r["bm"] for r in rungs] == [1, 2, 4, 8]
+    for M in (1, 2, 3, 5, 8):
+        A, B = synth.gemm_inputs(M, N, K, "bf16", bl, kind="int", seed=60 + M)
+        want = _round_to(oracle.gemm(A, B, bl), out)
+        for r in rungs:
+            if M > r["bm"]:
+                with pytest.raises(vx.VxError):
+                    p.gemm(A.cuda(), B.cuda(), force=(r["rung_id"], 1))
+                continue
+            got, _ = _run(p, A, B, force=(r["rung_id"], 1))
+            assert np.array_equal(got, want), (bl, out, M, r["bm"])
+    pb = vx.Plan(0, 64, "bf16", "fp32", "nk")
+    g = [r for r in pb.dump()["rungs"] if r["family"] == 3 and r["bm"] == 4][0]
+    Q, Kt = synth.gemm_inputs(3, 40, 64, "bf16", "nk", kind="int", seed=9, batch=5)
+    got, _ = _run(pb, Q, Kt, force=(g["rung_id"], 1))
+    assert np.array_equal(got, oracle.gemm(Q, Kt, "nk"))

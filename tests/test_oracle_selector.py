@@ -90,6 +90,9 @@ def test_table_invariants(K):
     assert t["rungs"], "empty strategy table"
     kb = S.ceil_div(K, S.BK_TC)
     for r in t["rungs"]:
+        if r["family"] == 3:                             # CUDA-core GEMV rungs (R20)
+            assert r["bm"] in S.GEMV_MT and r["splits"] == [1]
+            continue
         # divisibility down the chain (padding confined to the outermost level, Fig. padding)
         assert r["bm"] % r["um"] == 0 and r["bn"] % r["un"] == 0 and r["bk"] % S.UMMA_K == 0
         assert S.isa_compatible_f16((r["um"], r["un"], S.UMMA_K))
@@ -112,6 +115,8 @@ def _brute_best(t, batch, M, N, K):
         for s in r["splits"]:
             if s == 0 and not S.streamk_admissible(r, batch, M, N, DESC):   # R19
                 continue
+            if r["family"] == 3 and M > r["bm"]:                            # R20
+                continue
             c = S.rung_cost(r, s, batch, M, N, K, t["in"], t["out"], DESC, CAL)
             allc.append((c["cost"], c["padded_work"], r["rung_id"], s))
     return min(allc)
@@ -132,6 +137,8 @@ def test_select_is_argmin(N, K):
 def test_zero_padding_on_tile_multiples():
     t = S.build_table(4096, "bf16", "bf16", DESC)
     for r in t["rungs"]:
+        if r["family"] == 3:
+            continue                                   # GEMV rungs cover M <= MT only
         c = S.rung_cost(r, 1, 1, 128 * 40, 256 * 43, 4096, "bf16", "bf16", DESC, CAL)
         mt, nt = (256 * 43, 128 * 40) if r["swap"] else (128 * 40, 256 * 43)
         if mt % r["bm"] == 0 and nt % r["bn"] == 0:
@@ -176,6 +183,6 @@ def test_streamk_only_for_few_waves():
         if ch["split"] == 0:
             r = t["rungs"][ch["rung_id"]]
             assert S.streamk_admissible(r, 1, M, 11008, DESC)
-    big = [r for r in t["rungs"] if r["cg"] == 2][0]
+    big = [r for r in t["rungs"] if r["cg"] == 2 and r["family"] == 0][0]
     assert not S.streamk_admissible(big, 1, 16384, 11008, DESC)
     assert S.streamk_admissible(big, 1, 512, 11008, DESC)

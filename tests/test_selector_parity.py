@@ -23,8 +23,8 @@ BASELINE_NK = [(768, 768), (2304, 768), (3072, 768), (4096, 4096), (11008, 4096)
 FIELDS = ("rung_id", "split", "tiles_m", "tiles_n", "grid", "cost")
 
 
-def _oracle_table(K, i, o):
-    return S.build_table(K, i, o, DESC_J)
+def _oracle_table(K, i, o, bl="nk"):
+    return S.build_table(K, i, o, DESC_J, bl)
 
 
 def _lib_rungs(dump):
@@ -101,7 +101,11 @@ def test_forced_cost_matches_oracle():
     t = _oracle_table(768, "bf16", "bf16")
     for r in t["rungs"]:
         for s in r["splits"]:
-            for M in (1, 77, 512, 4096):
+            for M in (1, 2, 5, 8, 77, 512, 4096):
+                if r["family"] == 3 and M > r["bm"]:      # GEMV rung holds M <= MT (R20)
+                    with pytest.raises(vx.VxError):
+                        p.cost(r["rung_id"], s, M)
+                    continue
                 a = p.cost(r["rung_id"], s, M)
                 b = S.rung_cost(r, s, 1, M, 3072, 768, "bf16", "bf16", DESC_J, CAL)
                 assert a["cost"] == b["cost"] and a["grid"] == b["grid"]

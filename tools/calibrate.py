@@ -42,6 +42,8 @@ def measure(args):
         rungs = p.dump()["rungs"]
         for M in CAL_M:
             for r in rungs:
+                if r["family"] == 3 and M > r["bm"]:
+                    continue
                 for s in r["splits"]:
                     t = time_graph(p, 1, M, N, K, r["rung_id"], s, dev, stream, l2, 3, "nk")
                     out["samples"].append({"M": M, "N": N, "K": K, "rung": r["rung_id"],
@@ -62,6 +64,19 @@ def model_us(sm, th, desc, g):
     the fitted constants are judged by exactly the decisions vx_plan_select will make."""
     M, N, K, s = sm["M"], sm["N"], sm["K"], sm["split"]
     bm, bn, bk = sm["bm"], sm["bn"], 64
+    if sm["family"] == 3:   # CUDA-core GEMV rung (R20)
+        mac, l2s, epi = (int(round(th[k] * 1000)) for k in ("mac", "l2s", "epi"))
+        hbm = int(round(g["hbm"] * 1000))
+        t = lambda nbytes, bw: _cd(nbytes * 1000, bw)
+        bk = 256
+        tiles = _cd(N, bn)
+        F = _cd(tiles, desc["sm_count"] * 4)
+        trips = _cd(K, bk)
+        inner = t(bm * bn * bk, mac)
+        tl = max(t(bn * bk * 2 + bm * bk * 2, l2s), t(2 * K * (N + M), F * trips * hbm))
+        ts = max(t(bm * bn * 2, epi), t(2 * M * N, F * hbm))
+        cyc = F * (tl + (trips - 1) * max(tl, inner) + inner + ts) + int(round(th["fixed"]))
+        return cyc / (CLOCK_GHZ * 1e3)
     mac, l2s, epi = (int(round(th[k] * 1000)) for k in ("mac", "l2s", "epi"))
     fixed = int(round(th["fixed"]))
     hbm, dsm, skfix = (int(round(g[k] * 1000)) for k in ("hbm", "dsm", "skfix"))
@@ -111,7 +126,8 @@ def fit(args):
     raw = json.load(open(args.raw))
     desc = raw["desc"]
     S = raw["samples"]
-    keys = sorted({("umma_swap" if x["family"] == 1 else "umma", x["bm"], x["bn"]) for x in S})
+    fam = {0: "umma", 1: "umma_swap", 3: "gemv"}
+    keys = sorted({(fam[x["family"]], x["bm"], x["bn"]) for x in S})
     ini0 = json.load(open(args.init)) if args.init else None
     names = ["%s_%dx%d" % k for k in keys]
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -141,7 +157,7 @@ def fit(args):
         return th, g
 
     def key_of(x):
-        return "%s_%dx%d" % ("umma_swap" if x["family"] == 1 else "umma", x["bm"], x["bn"])
+        return "%s_%dx%d" % (fam[x["family"]], x["bm"], x["bn"])
 
     groups = {}
     for sm in S:
@@ -163,9 +179,13 @@ def fit(args):
         return e + args.regret_weight * r / len(groups)
 
     lo, hi = [], []
-    for _ in keys:
-        lo += [math.log(1000), math.log(8), math.log(8), math.log(500)]
-        hi += [math.log(4096), math.log(160), math.log(512), math.log(12000)]
+    for k in keys:
+        if k[0] == "gemv":
+            lo += [math.log(8), math.log(4), math.log(4), math.log(200)]
+            hi += [math.log(512), math.log(256), math.log(512), math.log(12000)]
+        else:
+            lo += [math.log(1000), math.log(8), math.log(8), math.log(500)]
+            hi += [math.log(4096), math.log(160), math.log(512), math.log(12000)]
     lo += [math.log(2), math.log(1), math.log(1)]
     hi += [math.log(64), math.log(8000), math.log(256)]
     x0 = [min(max(v, a), b) for v, a, b in zip(x0, lo, hi)]
