@@ -150,6 +150,8 @@ def main():
                  "forced": []}
         if not args.selected_only:
             for r in p.dump()["rungs"]:
+                if r["family"] == 3 and M > r["bm"]:   # GEMV rungs hold M <= MT (R20)
+                    continue
                 for s in r["splits"]:
                     run(r["rung_id"], s)
                     t = timed(r["rung_id"], s)
