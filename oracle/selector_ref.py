@@ -144,8 +144,8 @@ SIMT_TILES = ((32, 32, 2, 4), (64, 64, 4, 4), (128, 64, 8, 4))
 SIMT_BK = 16
 FAMILY_NAMES = {0: "umma", 1: "umma_swap", 2: "simt", 3: "gemv"}
 GEMV_MT = (1, 2, 4, 8)         # adaptive backend (R20): CUDA-core rungs for M <= MT
-GEMV_COLS = 32                 # 8 warps x 4 columns per CTA
-GEMV_BK = 256                  # k per warp iteration
+GEMV_COLS = 8                  # 2 column groups x 4 columns per CTA (x 4 K-slice warps)
+GEMV_BK = 1024                 # k per CTA step (4 K slices x 256)
 GEMV_OCC = 4                   # resident CTAs per SM assumed by the cost model
 
 
@@ -331,8 +331,8 @@ def rung_cost(rung: dict, s: int, batch: int, M: int, N: int, K: int,
 
 
 def _gemv_cost(rung, batch, M, N, K, in_b, out_b, desc, calib, cal):
-    """CUDA-core GEMV rung (R20): a CTA holds MT rows x 32 columns and walks K in steps of
-    256; GEMV_OCC CTAs per SM; Eqs. 2-4 as for the other rungs."""
+    """CUDA-core GEMV rung (R20): a CTA holds MT rows x 8 columns and walks K in steps of
+    1024; GEMV_OCC CTAs per SM; Eqs. 2-4 as for the other rungs."""
     bm, bn, bk = rung["bm"], rung["bn"], rung["bk"]
     hbm = calib["hbm_milli"]
     tiles = batch * ceil_div(N, bn)

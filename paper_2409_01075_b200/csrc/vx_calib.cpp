@@ -38,10 +38,10 @@ static const RungCalib kRungs[] = {
     {"umma_swap_128x32", 1000000, 35009, 17712, 2940},
     {"umma_swap_128x64", 1217391, 46467, 507952, 7173},
     {"umma_swap_128x128", 1449009, 160000, 512000, 1975},
-    {"gemv_1x32", 64000, 32000, 16000, 1500},
-    {"gemv_2x32", 64000, 32000, 16000, 1500},
-    {"gemv_4x32", 64000, 32000, 16000, 1500},
-    {"gemv_8x32", 64000, 32000, 16000, 1500},
+    {"gemv_1x8", 64000, 32000, 16000, 1500},
+    {"gemv_2x8", 64000, 32000, 16000, 1500},
+    {"gemv_4x8", 64000, 32000, 16000, 1500},
+    {"gemv_8x8", 64000, 32000, 16000, 1500},
     {"simt_32x32", 128000, 32000, 16000, 2000},
     {"simt_64x64", 128000, 32000, 16000, 2000},
     {"simt_128x64", 128000, 32000, 16000, 2000},

@@ -23,8 +23,8 @@ constexpr int kSmemReserve = 2048; // barriers + 1024-B alignment slack
 constexpr int kEpiStaging = 32768; // epilogue: 4 warps x 2 x 4 KB TMA-store staging tiles
 constexpr int kClusterMax = 8;     // portable cluster size
 constexpr int kSimtBk = 16;
-constexpr int kGemvBk = 256;        // k per warp iteration (32 lanes x 8 elements)
-constexpr int kGemvColsPerCta = 32; // 8 warps x 4 columns
+constexpr int kGemvBk = 1024;       // k per CTA step (4 K-slice warps x 32 lanes x 8 elements)
+constexpr int kGemvColsPerCta = 8;  // 2 column groups x 4 columns (x 4 K slices = 8 warps)
 constexpr int kGemvOcc = 4;         // resident CTAs per SM assumed by the cost model (R20)
 
 // One rung = one full chain L0 -> L1 -> L2 -> L3 of the strategy table (Alg. 2 map).

@@ -226,7 +226,7 @@ static void rung_cost(const vx_plan_s* p, const Rung& r, int s, int64_t batch, i
     const int64_t tiles = batch * tm * tn;
     const int64_t kb = cdiv(K, bk);
     if (r.family == kGemv) {
-        // CUDA-core GEMV rung (R20): a CTA = MT rows x 32 columns; k-steps of 256
+        // CUDA-core GEMV rung (R20): a CTA = MT rows x 8 columns; k-steps of 1024
         const int64_t tiles_g = batch * cdiv(N, bn);
         const int64_t slots_g = (int64_t)d.sm_count * kGemvOcc;
         const int64_t Fg = eq3(tiles_g, slots_g);

@@ -21,7 +21,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-CAL_M = (1, 8, 32, 64, 128, 200, 384, 512, 768, 1024, 1536, 2048, 3072, 4096, 8192)
+CAL_M = (1, 2, 4, 8, 32, 64, 128, 200, 384, 512, 768, 1024, 1536, 2048, 3072, 4096, 8192)
 # generic (N, K): powers of two and N with odd tile counts (13 / 21 / 42 tiles of 256)
 CAL_NK = ((1024, 1024), (4096, 1024), (2048, 4096), (8192, 4096), (6144, 2048),
           (3328, 1536), (5376, 4096), (10752, 2048))
@@ -68,7 +68,7 @@ def model_us(sm, th, desc, g):
         mac, l2s, epi = (int(round(th[k] * 1000)) for k in ("mac", "l2s", "epi"))
         hbm = int(round(g["hbm"] * 1000))
         t = lambda nbytes, bw: _cd(nbytes * 1000, bw)
-        bk = 256
+        bk = 1024
         tiles = _cd(N, bn)
         F = _cd(tiles, desc["sm_count"] * 4)
         trips = _cd(K, bk)

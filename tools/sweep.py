@@ -156,7 +156,7 @@ def main():
                     run(r["rung_id"], s)
                     t = timed(r["rung_id"], s)
                     c = p.cost(r["rung_id"], s, M, N=N, batch=batch)
-                    entry["forced"].append({"rung": r["rung_id"], "split": s, "us": t,
+                    entry["forced"].append({"rung": r["rung_id"], "family": r["family"], "split": s, "us": t,
                                             "cost": c["cost"]})
             best = min(entry["forced"], key=lambda e: e["us"])
             entry["best"] = best
