@@ -37,6 +37,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
+// one elected lane of a converged warp (the lowest active lane): lets a whole warp run a
+// role's loop with warp-uniform values (uniform datapath, no per-lane R2UR waterfall
+// around tcgen05 instructions) while exactly one thread issues
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}"
+        : "=r"(pred));
+    return pred != 0;
+}
+
 // ---- TMA ---------------------------------------------------------------------------------
 __device__ __forceinline__ void prefetch_tmap(const void* tmap) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
@@ -50,6 +61,15 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const void* tmap, uint64_
         "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_addr(bar)),
         "l"(policy)
         : "memory");
+}
+// 3-D tile prefetch global -> L2 (no shared-memory destination, no completion).  L2 is
+// the coherence point, so this is safe even while a preceding grid may still write the
+// tile: a later write updates the L2 line.
+__device__ __forceinline__ void tma_prefetch_3d(const void* tmap, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                     reinterpret_cast<uint64_t>(tmap)),
+                 "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
 }
 // 3-D tile store shared -> global (bulk-group completion); OOB elements are not written
 __device__ __forceinline__ void tma_store_3d(const void* tmap, const void* src, int c0, int c1,

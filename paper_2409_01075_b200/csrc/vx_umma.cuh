@@ -34,7 +34,14 @@ namespace vx {
 constexpr int kEpiWarp0 = 2;
 constexpr int kEpiWarps = 8;   // two warps per TMEM lane quarter, splitting the column chunks
 constexpr int kEpiThreads = kEpiWarps * 32;
-constexpr int kThreads = kEpiWarp0 * 32 + kEpiThreads;
+// TMA producers: warp 0 and warp 10 take alternate k-blocks.  One thread issues a
+// UTMALDG only every ~70-160 cycles plus ~70 for its mbarrier wait (tools/tma_bench.cu),
+// so a single producer caps a CTA at ~0.26 us per 64-deep k-block whatever the tile size;
+// two halve that and leave the 128xBN tiles MMA- or bandwidth-bound.
+constexpr int kProdWarps = 2;
+constexpr int kProdWarp1 = kEpiWarp0 + kEpiWarps;          // the second producer warp
+constexpr int kThreads = (kEpiWarp0 + kEpiWarps + kProdWarps - 1) * 32;
+__device__ __forceinline__ bool is_epi_warp(int w) { return w >= kEpiWarp0 && w < kEpiWarp0 + kEpiWarps; }
 
 struct UmmaParams {
     int M, N;                 // logical GEMM rows / cols (per batch)
@@ -130,12 +137,13 @@ __device__ __forceinline__ void epi_bar() {   // named barrier over the 8 epilog
     asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
 }
 
-// phase trace (tracing aux subsystem): %globaltimer (ns) at fixed points, 8 slots per CTA
+// phase trace (tracing aux subsystem): %globaltimer (ns) at fixed points, 16 slots per CTA
+// (slots 12-15: MMA-issuer cycle counters, see the MMA loop)
 __device__ __forceinline__ void trace_at(const UmmaParams& p, int slot) {
     if (p.trace) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        p.trace[blockIdx.x * 8 + slot] = t;
+        p.trace[blockIdx.x * 16 + slot] = t;
     }
 }
 
@@ -319,7 +327,7 @@ __device__ __forceinline__ void sk_reset(const UmmaParams& p, int c0, int c1, ui
 template <int BN, bool SWAP, bool P_MN, bool Q_MN, bool PAIR = false>
 __global__ void __launch_bounds__(kThreads, 1)
     vx_umma_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmQ,
-                   const __grid_constant__ CUtensorMap tmC, const UmmaParams p) {
+                   const __grid_constant__ CUtensorMap tmC, const __grid_constant__ UmmaParams p) {
     static_assert(!PAIR || !SWAP, "pair rungs are non-swapped");
     using Cfg = UmmaCfg<BN>;
     constexpr int kP = Cfg::kPBytes;
@@ -361,6 +369,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (PAIR) ptx::tmem_alloc_pair<Cfg::kTmemCols>(tmem_holder);
         else ptx::tmem_alloc<Cfg::kTmemCols>(tmem_holder);
     }
+    if (warp == 0 && lane == 0 && !(p.dbg & 128) && !p.bpack && !P_MN && !Q_MN) {
+        // L2 prefetch of this CTA's first ring-full of P and Q tiles, before the grid
+        // dependency wait: the first loads after it then hit L2 instead of DRAM
+        const int rk = p.splits > 1 ? (int)(blockIdx.x % p.splits) : 0;
+        const int pr = PAIR ? (int)ptx::cluster_ctarank() : 0;
+        WorkIter w0(p, rk);
+        int t, k0, nk;
+        if (w0.next(p, t, k0, nk)) {
+            int b, tp, tq;
+            decode_tile(t, p.tiles_p, p.tiles_q, b, tp, tq);
+            const int pp = PAIR ? tp * 256 + pr * 128 : tp * 128;
+            const int qq = PAIR ? tq * BN + pr * (BN / 2) : tq * BN;
+            const int n = nk < S ? nk : S;
+            for (int kb = k0; kb < k0 + n; ++kb) {
+                ptx::tma_prefetch_3d(&tmP, kb * 64, pp, b);
+                ptx::tma_prefetch_3d(&tmQ, kb * 64, qq, b);
+            }
+        }
+    }
     ptx::tc_fence_before();
     if (PAIR) ptx::cluster_sync();   // both CTAs' barriers initialised before any remote use
     else __syncthreads();
@@ -371,24 +398,33 @@ __global__ void __launch_bounds__(kThreads, 1)
     // everything above (barrier init, TMEM alloc, descriptor prefetch) overlaps the previous
     // kernel under PDL; no global memory is touched before this point
     ptx::grid_dep_wait();
+    if (threadIdx.x == 0) trace_at(p, 8);
 
     const bool split = p.splits > 1;
     const int rank = split ? (int)(blockIdx.x % p.splits) : 0;
     const int tile0 = split ? (int)(blockIdx.x / p.splits) : (int)blockIdx.x;  // split mode
 
-    if (warp == 0) {
+    if (warp == 0 || warp == kProdWarp1) {
         if (lane == 0) {
-            // ===== TMA producer =====
+            // ===== TMA producers: producer `pid` takes this CTA's k-blocks j % 2 == pid =====
+            const int pid = warp == 0 ? 0 : 1;
             const uint64_t pol = ptx::policy_evict_last();
             int stage = 0;
             uint32_t phase = 0;
+            bool stamped = pid != 0;
+            int j = 0;                       // running k-block count of this CTA
             WorkIter wi(p, rank);
             int tile, k0, nk;
             while (wi.next(p, tile, k0, nk)) {
                 int b, tp, tq;
                 decode_tile(tile, p.tiles_p, p.tiles_q, b, tp, tq);
-                for (int kb = k0; kb < k0 + nk; ++kb) {
+                for (int kb = k0; kb < k0 + nk; ++kb, ++j) {
+                    if (j % kProdWarps != pid) {
+                        if (++stage == S) { stage = 0; phase ^= 1; }
+                        continue;
+                    }
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
+                    if (kb >= k0 + kProdWarps && !stamped) { trace_at(p, 10); stamped = true; }
                     uint8_t* dP = sP + stage * kP;
                     uint8_t* dQ = sQ + stage * kQ;
                     if (PAIR) {
@@ -416,6 +452,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         continue;
                     }
                     ptx::mbar_arrive_expect_tx(&full[stage], kP + kQ);
+                    if (!stamped && kb == k0) trace_at(p, 11);
                     if (p.bpack) {
                         // B pre-packed: every 64-row block of the B tile is one 8-KB box
                         if (SWAP) {
@@ -454,11 +491,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
             ptx::grid_dep_launch();  // all loads issued: let the next grid start its prologue
-            trace_at(p, 2);
+            if (pid == 0) trace_at(p, 2);
         }
     } else if (warp == 1) {
-        if (lane == 0 && prank == 0) {
-            // ===== MMA issuer (single thread; the pair leader for PAIR rungs) =====
+        if (prank == 0) {
+            // ===== MMA issuer: the whole warp walks the loop (warp-uniform operands), one
+            // elected lane issues (the pair leader's warp for PAIR rungs) =====
+            long long cyc_wait = 0, cyc_mma = 0, cyc_commit = 0, cyc_n = 0;   // trace only
+            const bool tr = p.trace != nullptr;
+            const uint32_t idesc = p.idesc;
+            const bool mma_off = (p.dbg & 512) != 0;   // debug: TMA streaming only
             int stage = 0;
             uint32_t phase = 0;
             int it = 0;
@@ -471,33 +513,57 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
                 for (int i = 0; i < nk; ++i) {
+                    const long long c0 = tr ? clock64() : 0;
                     ptx::mbar_wait(&full[stage], phase);
                     ptx::tc_fence_after();
-                    if (it == 0 && i == 0) trace_at(p, 3);
+                    const long long c1 = tr ? clock64() : 0;
+                    if (it == 0 && i == 0 && lane == 0) trace_at(p, 3);
                     const uint32_t aP = ptx::smem_addr(sP + stage * kP);
                     const uint32_t aQ = ptx::smem_addr(sQ + stage * kQ);
+                    long long c2 = 0;
+                    if (ptx::elect_one()) {
+                        if (!mma_off) {
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        // K-major: +32 B inside the swizzle row; MN-major: +2 K-groups (2 KB)
-                        const uint64_t dp = P_MN ? ptx::sdesc_mn_sw128(aP + k * 2048, 8192)
-                                                 : ptx::sdesc_k_sw128(aP + k * 32);
-                        const uint64_t dq = Q_MN ? ptx::sdesc_mn_sw128(aQ + k * 2048, 8192)
-                                                 : ptx::sdesc_k_sw128(aQ + k * 32);
-                        if (PAIR) ptx::umma_f16_pair(d_tmem, dp, dq, p.idesc, (i | k) != 0);
-                        else ptx::umma_f16(d_tmem, dp, dq, p.idesc, (i | k) != 0);
+                            for (int k = 0; k < 4; ++k) {
+                                // K-major: +32 B inside the swizzle row; MN-major: +2 K-groups
+                                const uint64_t dp = P_MN ? ptx::sdesc_mn_sw128(aP + k * 2048, 8192)
+                                                         : ptx::sdesc_k_sw128(aP + k * 32);
+                                const uint64_t dq = Q_MN ? ptx::sdesc_mn_sw128(aQ + k * 2048, 8192)
+                                                         : ptx::sdesc_k_sw128(aQ + k * 32);
+                                if (PAIR) ptx::umma_f16_pair(d_tmem, dp, dq, idesc, (i | k) != 0);
+                                else ptx::umma_f16(d_tmem, dp, dq, idesc, (i | k) != 0);
+                            }
+                        }
+                        c2 = tr ? clock64() : 0;
+                        // frees the stage (in both CTAs of a pair) when these MMAs finish
+                        if (PAIR) ptx::umma_commit_pair(&empty[stage], 3);
+                        else ptx::umma_commit(&empty[stage]);
+                        if (tr) {
+                            const long long c3 = clock64();
+                            cyc_wait += c1 - c0; cyc_mma += c2 - c1; cyc_commit += c3 - c2; ++cyc_n;
+                        }
                     }
-                    // frees the stage (in both CTAs of a pair) when these MMAs finish
-                    if (PAIR) ptx::umma_commit_pair(&empty[stage], 3);
-                    else ptx::umma_commit(&empty[stage]);
+                    __syncwarp();
                     if (++stage == S) { stage = 0; phase ^= 1; }
                 }
                 // accumulator ready for the epilogue (of both CTAs of a pair)
-                if (PAIR) ptx::umma_commit_pair(&tfull[acc], 3);
-                else ptx::umma_commit(&tfull[acc]);
+                if (ptx::elect_one()) {
+                    if (PAIR) ptx::umma_commit_pair(&tfull[acc], 3);
+                    else ptx::umma_commit(&tfull[acc]);
+                }
+                __syncwarp();
             }
-            trace_at(p, 4);
+            if (lane == 0) {
+                trace_at(p, 4);
+                if (tr) {
+                    p.trace[blockIdx.x * 16 + 12] = cyc_wait;
+                    p.trace[blockIdx.x * 16 + 13] = cyc_mma;
+                    p.trace[blockIdx.x * 16 + 14] = cyc_commit;
+                    p.trace[blockIdx.x * 16 + 15] = cyc_n;
+                }
+            }
         }
-    } else {
+    } else if (is_epi_warp(warp)) {
         // ===== epilogue warps =====
         // warp w reads TMEM lanes 32*(w%4)..+31 (its quarter of the tile rows); the two
         // warps of a quarter (group g = 0, 1) take alternate column chunks
@@ -695,7 +761,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane == 0) release_acc(&tempty[acc]);
             if (c_last >= c_first) sk_reset<PAIR>(p, c_first, c_last, prank);
         }
-        if (lane == 0) ptx::bulk_wait<0>();   // TMA stores complete before the CTA retires
+        // TMA stores have read their staging before the CTA retires (the grid completes only
+        // once the stores are performed, which is what the next grid's wait observes)
+        if (lane == 0) {
+            if (p.dbg & 256) ptx::bulk_wait<0>();
+            else ptx::bulk_wait_read<0>();
+        }
     }
 
     __syncwarp();  // reconverge the single-lane roles before the .aligned cluster barriers
@@ -713,7 +784,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t red_addr = ptx::smem_addr(sP);
         ptx::cluster_sync();
         ptx::tc_fence_after();
-        if (warp >= kEpiWarp0 && !(p.dbg & 1)) {
+        if (is_epi_warp(warp) && !(p.dbg & 1)) {
             const int quarter = warp & 3;
             const int row = quarter * 32 + lane;
             const int owner = row / rows;
@@ -737,7 +808,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         ptx::cluster_sync();
         if (threadIdx.x == kEpiWarp0 * 32) trace_at(p, 6);
-        if (warp >= kEpiWarp0 && !(p.dbg & 2)) {
+        if (is_epi_warp(warp) && !(p.dbg & 2)) {
             int b, tp, tq;
             decode_tile(tile0, p.tiles_p, p.tiles_q, b, tp, tq);
             const int et = threadIdx.x - kEpiWarp0 * 32;
@@ -792,6 +863,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tc_fence_after();
         if (PAIR) ptx::tmem_dealloc_pair<Cfg::kTmemCols>(tmem_base);
         else ptx::tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+        if (lane == 0) trace_at(p, 9);
     }
 }
 

@@ -167,10 +167,14 @@ def fit(args):
     def loss(x):
         th, g = unpack(x)
         e = 0.0
+        n = 0
         for sm in S:
             pred = model_us(sm, th[key_of(sm)], desc, g)
+            if pred == float("inf"):      # inadmissible (R19): never selected, not fitted
+                continue
             e += (math.log(pred) - math.log(sm["us"])) ** 2
-        e = args.err_weight * e / len(S)
+            n += 1
+        e = args.err_weight * e / max(n, 1)
         # selection quality: log-regret of the model's pick per calibration shape
         r = 0.0
         for k, v in groups.items():

@@ -6,7 +6,9 @@ import numpy as np, torch
 import paper_2409_01075_b200 as vx
 import synth
 
-PH = ["entry", "setup", "prod_done", "first_full", "mma_done", "acc_ready", "epi/sync2", "reduced"]
+PH = ["entry", "setup", "prod_done", "first_full", "mma_done", "acc_ready", "epi/sync2", "reduced",
+      "dep_released", "exit", "first_issue", "-"]
+NS = 16        # slots per CTA (vx_umma.cuh trace_at)
 
 def main():
     a = [x for x in sys.argv[1:] if not x.startswith("--")]
@@ -17,7 +19,7 @@ def main():
     A = synth.matrix((M, K), "bf16", seed=1, device=dev)
     B = synth.matrix((N, K), "bf16", seed=2, scale=K ** -0.5, device=dev)
     C = torch.empty((M, N), dtype=torch.bfloat16, device=dev)
-    buf = torch.zeros(8 * 4096, dtype=torch.int64, device=dev)
+    buf = torch.zeros(NS * 4096, dtype=torch.int64, device=dev)
     fl = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     vx.lib.vx_debug_set_trace.argtypes = [ctypes.c_void_p]
     sp = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
@@ -35,7 +37,7 @@ def main():
         vx.lib.vx_debug_set_trace(None)
         assert st == 0, vx.lib.vx_last_error()
     g = ch.grid
-    t = buf[: 8 * g].view(g, 8).cpu().numpy().astype(np.int64)
+    t = buf[: NS * g].view(g, NS).cpu().numpy().astype(np.int64)
     t0 = t[:, 0].min()
     rel = (t - t0) / 1000.0
     print("M=%d N=%d K=%d choice=%s event=%.2fus" % (M, N, K, ch.as_dict(), e0.elapsed_time(e1) * 1e3))
