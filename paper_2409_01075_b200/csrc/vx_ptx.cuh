@@ -295,6 +295,16 @@ __device__ __forceinline__ void st_dsmem_f4(uint32_t addr, float a, float b, flo
                  "f"(c), "f"(d)
                  : "memory");
 }
+// asynchronous 16-B store into another CTA's shared memory; its bytes complete_tx on that
+// CTA's mbarrier (no cluster barrier needed for visibility)
+__device__ __forceinline__ void st_async_f4(uint32_t addr, uint32_t remote_bar, uint32_t a, uint32_t b,
+                                            uint32_t c, uint32_t d) {
+    asm volatile(
+        "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+            addr),
+        "r"(a), "r"(b), "r"(c), "r"(d), "r"(remote_bar)
+        : "memory");
+}
 // arrive (release, cluster scope) on an mbarrier of another CTA of the cluster
 __device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)

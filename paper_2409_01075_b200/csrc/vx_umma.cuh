@@ -137,13 +137,14 @@ __device__ __forceinline__ void epi_bar() {   // named barrier over the 8 epilog
     asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
 }
 
-// phase trace (tracing aux subsystem): %globaltimer (ns) at fixed points, 16 slots per CTA
+constexpr int kTraceSlots = 20;
+// phase trace (tracing aux subsystem): %globaltimer (ns) at fixed points, 20 slots per CTA
 // (slots 12-15: MMA-issuer cycle counters, see the MMA loop)
 __device__ __forceinline__ void trace_at(const UmmaParams& p, int slot) {
     if (p.trace) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        p.trace[blockIdx.x * 16 + slot] = t;
+        p.trace[blockIdx.x * kTraceSlots + slot] = t;
     }
 }
 
@@ -344,7 +345,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* empty = full + S;
     uint64_t* tfull = empty + S;
     uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* redbar = tempty + 2;   // split mode: the peers' partial rows have landed
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(redbar + 1);
     const uint32_t raw_addr = ptx::smem_addr(smem_raw);
     const uint32_t tile_off = ((raw_addr + 512 + 1023) & ~1023u) - raw_addr;
     uint8_t* sP = smem_raw + tile_off;
@@ -363,6 +365,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_init(&tfull[i], 1);
             ptx::mbar_init(&tempty[i], PAIR ? 2 * kEpiWarps : kEpiWarps);
         }
+        ptx::mbar_init(redbar, 1);
         ptx::fence_mbar_init();
     }
     if (warp == 1) {
@@ -556,10 +559,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane == 0) {
                 trace_at(p, 4);
                 if (tr) {
-                    p.trace[blockIdx.x * 16 + 12] = cyc_wait;
-                    p.trace[blockIdx.x * 16 + 13] = cyc_mma;
-                    p.trace[blockIdx.x * 16 + 14] = cyc_commit;
-                    p.trace[blockIdx.x * 16 + 15] = cyc_n;
+                    p.trace[blockIdx.x * kTraceSlots + 12] = cyc_wait;
+                    p.trace[blockIdx.x * kTraceSlots + 13] = cyc_mma;
+                    p.trace[blockIdx.x * kTraceSlots + 14] = cyc_commit;
+                    p.trace[blockIdx.x * kTraceSlots + 15] = cyc_n;
                 }
             }
         }
@@ -773,40 +776,60 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (!split && threadIdx.x == kEpiWarp0 * 32) trace_at(p, 6);
     if (split) {
         // deterministic in-cluster reduce-scatter of the s K-slice partials (R7):
-        //  (1) cluster barrier: every CTA's MMAs are complete, so every SMEM ring is free;
-        //  (2) each epilogue thread reads its accumulator row from TMEM and posts it with
-        //      st.shared::cluster into slot [my rank] of the CTA owning that row (rows are
-        //      owned in blocks of 128/s);
-        //  (3) cluster barrier (release/acquire: the posted rows are visible);
-        //  (4) each CTA sums its rows over slots 0..s-1 in rank order and stores C.
-        constexpr int RS = BN + 4;                  // padded row stride (floats)
-        const int rows = 128 / p.splits;
+        //  (1) the owner thread of each CTA posts the byte count it expects from its peers
+        //      on `redbar`, then a cluster barrier: every CTA's MMAs are complete, so every
+        //      SMEM ring is free to receive;
+        //  (2) each epilogue thread reads its accumulator row from TMEM; rows are owned in
+        //      blocks of 128/s; a row it owns goes to its own slot [rank] with st.shared, a
+        //      peer's row goes to slot [rank] of the owner with st.async, whose bytes
+        //      complete on the owner's `redbar` (no second cluster barrier);
+        //  (3) each CTA waits for its own and its peers' rows, sums its rows over slots
+        //      0..s-1 in rank order and stores C.
+        // slot layout (floats): [src rank][32-col chunk c][row rr][W], 16-B groups XOR-
+        // swizzled by the row so the row-per-lane stores and the reads are conflict-light.
+        constexpr int W = BN >= 32 ? 32 : BN;     // columns per chunk
+        constexpr int G = W / 4;                  // 16-B groups per chunk row
+        const int s_ = p.splits;
+        const int rows = 128 / s_;
+        const int slot = rows * BN;               // floats per source-rank slot
         const uint32_t red_addr = ptx::smem_addr(sP);
+        const bool post = !(p.dbg & 1);
+        if (threadIdx.x == kEpiWarp0 * 32 && post)
+            ptx::mbar_arrive_expect_tx(redbar, (uint32_t)((s_ - 1) * slot * 4));
         ptx::cluster_sync();
         ptx::tc_fence_after();
-        if (is_epi_warp(warp) && !(p.dbg & 1)) {
+        if (threadIdx.x == kEpiWarp0 * 32) trace_at(p, 16);
+        if (is_epi_warp(warp) && post) {
             const int quarter = warp & 3;
             const int row = quarter * 32 + lane;
             const int owner = row / rows;
-            const uint32_t dst = ptx::mapa(
-                red_addr + (uint32_t)(((rank * rows) + (row - owner * rows)) * RS) * 4u, owner);
+            const int rr = row - owner * rows;
+            const uint32_t base = red_addr + (uint32_t)(rank * slot + rr * W) * 4u;
+            const uint32_t dst = owner == rank ? base : ptx::mapa(base, owner);
+            const uint32_t rbar = ptx::mapa(ptx::smem_addr(redbar), owner);
             const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16);
             const int grp = (warp - kEpiWarp0) >> 2;
+            const int sw = G == 8 ? (rr & 7) : G == 4 ? ((rr >> 1) & 3) : 0;
 #pragma unroll 1
             for (int c = grp; c < (BN + 31) / 32; c += 2) {
                 uint32_t v[32];
                 if (BN >= 32) ptx::tmem_ld32(taddr + c * 32, v);
                 else ptx::tmem_ld16(taddr + c * 32, v);
                 ptx::tmem_wait_ld();
-                constexpr int W = BN >= 32 ? 32 : BN;
-                const float* f = reinterpret_cast<const float*>(v);
+                const uint32_t cd = dst + (uint32_t)(c * rows * W) * 4u;
 #pragma unroll
-                for (int j = 0; j < W; j += 4)
-                    ptx::st_dsmem_f4(dst + (uint32_t)(c * 32 + j) * 4u, f[j], f[j + 1], f[j + 2],
-                                     f[j + 3]);
+                for (int g = 0; g < G; ++g) {
+                    const uint32_t a = cd + (uint32_t)((g ^ sw) * 16);
+                    if (owner == rank) ptx::st_shared_v4(a, v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]);
+                    else ptx::st_async_f4(a, rbar, v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]);
+                }
             }
         }
-        ptx::cluster_sync();
+        if (threadIdx.x == kEpiWarp0 * 32) trace_at(p, 17);
+        if (is_epi_warp(warp)) {
+            epi_bar();                               // this CTA's own rows are in SMEM
+            if (post) ptx::mbar_wait(redbar, 0);     // the peers' rows too
+        }
         if (threadIdx.x == kEpiWarp0 * 32) trace_at(p, 6);
         if (is_epi_warp(warp) && !(p.dbg & 2)) {
             int b, tp, tq;
@@ -816,16 +839,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             char* Cb = reinterpret_cast<char*>(p.C) +
                        (long long)b * p.sC * (p.out_kind == 2 ? 4 : 2);
             const int n4 = BN / 4;
-            const int slot = rows * RS;             // floats per source-rank slot
 #pragma unroll 1
             for (int idx = et; idx < rows * n4; idx += kEpiThreads) {
                 int rr, cc;
                 if (SWAP) { rr = idx % rows; cc = (idx / rows) * 4; }   // consecutive n
                 else { rr = idx / n4; cc = (idx % n4) * 4; }            // consecutive n
-                const float* src = red + rr * RS + cc;
+                const int c = cc / W, g = (cc % W) / 4;
+                const int sw = G == 8 ? (rr & 7) : G == 4 ? ((rr >> 1) & 3) : 0;
+                const float* src = red + (c * rows + rr) * W + ((g ^ sw) * 4);
                 float4 acc4 = *reinterpret_cast<const float4*>(src);
 #pragma unroll 1
-                for (int j = 1; j < p.splits; ++j) {
+                for (int j = 1; j < s_; ++j) {
                     const float4 t = *reinterpret_cast<const float4*>(src + j * slot);
                     acc4.x += t.x; acc4.y += t.y; acc4.z += t.z; acc4.w += t.w;
                 }

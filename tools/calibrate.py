@@ -21,10 +21,10 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-CAL_M = (1, 2, 4, 8, 32, 64, 128, 200, 384, 512, 768, 1024, 1536, 2048, 3072, 4096, 8192)
+CAL_M = (1, 2, 4, 8, 16, 32, 64, 128, 200, 384, 512, 768, 1024, 1536, 2048, 3072, 4096, 8192)
 # generic (N, K): powers of two and N with odd tile counts (13 / 21 / 42 tiles of 256)
 CAL_NK = ((1024, 1024), (4096, 1024), (2048, 4096), (8192, 4096), (6144, 2048),
-          (3328, 1536), (5376, 4096), (10752, 2048))
+          (3328, 1536), (5376, 4096), (10752, 2048), (1536, 512), (2560, 640))
 CLOCK_GHZ = 1.965   # cycles of the model are SM cycles at the max clock
 
 
@@ -185,7 +185,7 @@ def fit(args):
     lo, hi = [], []
     for k in keys:
         if k[0] == "gemv":
-            lo += [math.log(8), math.log(4), math.log(4), math.log(200)]
+            lo += [math.log(1), math.log(4), math.log(1), math.log(200)]
             hi += [math.log(512), math.log(256), math.log(512), math.log(12000)]
         else:
             lo += [math.log(1000), math.log(8), math.log(8), math.log(500)]

@@ -2,7 +2,8 @@
 CUDA graph on rotating cold buffers (as tools/sweep.py --method graph), each launch with its
 own %globaltimer trace slice (vx_debug_set_trace).  Prints, per phase, the median over
 launches 1..R-1 of the time relative to the PREVIOUS launch's last CTA exit -- where the
-per-launch floor goes.
+per-launch floor goes.  NOTE: %globaltimer ticks every ~0.256 us on B200, so single phase
+stamps are quantised to that; cycle counters (slots 12-14) are exact.
 
     python tools/timeline.py M N K [rung split] [--R 32] [--hot]
 """
@@ -18,8 +19,8 @@ import paper_2409_01075_b200 as vx
 import synth
 
 PH = ["entry", "setup", "prod_done", "first_full", "mma_done", "acc_ready", "epi_done",
-      "pre_teardown", "dep_released", "exit", "2nd_issue", "1st_issue"]
-NS = 16   # slots per CTA; 12-15 = MMA-issuer cycle counters (wait, issue, commit, n)
+      "pre_teardown", "dep_released", "exit", "2nd_issue", "1st_issue", "-", "-", "-", "-", "split_sync1", "split_posted", "-", "-"]
+NS = 20   # slots per CTA; 12-15 = MMA-issuer cycle counters (wait, issue, commit, n)
 
 
 def main():
@@ -78,6 +79,8 @@ def main():
         prev_exit = t[i - 1, :, 9].max()
         per_launch.append((t[i, :, 9].max() - prev_exit) / 1e3)
         for j, nm in enumerate(PH):
+            if nm == "-":
+                continue
             col = t[i, :, j]
             col = col[col > 0]
             if len(col):
@@ -92,7 +95,7 @@ def main():
         print("  MMA issuer cycles per k-block: wait-full %.0f  issue %.0f  commit %.0f" % (
             np.median(cy[:, 0] / n), np.median(cy[:, 1] / n), np.median(cy[:, 2] / n)))
     for nm in PH:
-        if rows[nm]:
+        if nm != "-" and rows[nm]:
             v = np.median(np.array(rows[nm]), axis=0)
             print("  %-13s first %7.2f  median %7.2f  last %7.2f" % (nm, v[0], v[1], v[2]))
 
