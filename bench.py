@@ -272,6 +272,16 @@ class Arena:
         self.pos += (n + 127) // 128 * 128     # keep 256-B alignment
         return p
 
+    def take_view(self, rows, cols):
+        """Like take(), as a [rows, cols] tensor view (for the cuBLAS reference line)."""
+        n = rows * cols
+        assert n <= self.n
+        if self.pos + n > self.n:
+            self.pos = 0
+        v = self.t[self.pos:self.pos + n].view(rows, cols)
+        self.pos += (n + 127) // 128 * 128
+        return v
+
 
 class SweepGraph:
     """The whole sweep as ONE CUDA graph: for every point, an external event-record node,
@@ -410,6 +420,19 @@ def run_mine(args, rank, world, local):
 
     sharded = run_sharded(args, rank, world, local, vx, stream, side, l2)
     e2e = None if args.no_e2e else run_e2e(args, rank, world, local, vx, plans, pts, stream)
+    cublas = None
+    if world == 1 and not args.no_cublas:
+        t_cb = run_cublas_ref(pts, stream, side, rank, R_PER_POINT, max(3, args.steps // 2))
+        r_cb = [flops(M, N, K) / (ms * 1e-3) / 1e12 for (_, M, N, K), ms in zip(pts, t_cb)]
+        ratio = [ours / cb for ours, cb in zip(rates, r_cb)]
+        for row, ms in zip(rows, t_cb):
+            row["cublas_us"] = ms * 1e3
+        cublas = {"value": geomean(r_cb), "unit": UNIT,
+                  "kind": "torch.mm (cuBLAS %s) on the same points and timing; informational, "
+                          "not part of the library" % torch.backends.cuda.preferred_blas_library(),
+                  "ours_over_cublas_geomean": geomean(ratio),
+                  "points_ours_faster": sum(1 for x in ratio if x > 1.0), "points": len(ratio)}
+    selector = selector_overhead(vx, sorted(plans), local) if rank == 0 else None
 
     result = None
     if rank == 0:
@@ -444,6 +467,8 @@ def run_mine(args, rank, world, local):
             "sharded": sharded,
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "cublas_ref": cublas,
+            "selector": selector,
             "gpu_launches": launches,
             "clocks": clk,
         }
@@ -452,6 +477,72 @@ def run_mine(args, rank, world, local):
                 json.dump(rows, f, indent=1)
         print(json.dumps(result), flush=True)
     return result
+
+
+def run_cublas_ref(pts, stream, side, rank, R, steps):
+    """Informational B200 context line: torch.mm -> cuBLAS on the same
+    sweep points, same timing method (one graph per step, R launches per point on fresh
+    arena slices, events between points).  Not part of the library or its hot path."""
+    arenas = make_arenas(pts, stream.device, rank)
+    aA, aB, aC = arenas
+    work = [(M, N, K, [(aA.take_view(M, K), aB.take_view(N, K), aC.take_view(M, N))
+                       for _ in range(R)]) for _, M, N, K in pts]
+    side.wait_stream(stream)
+    with torch.cuda.stream(side):
+        for M, N, K, views in work:                       # cuBLAS heuristics / workspaces
+            a, b, c = views[0]
+            torch.mm(a, b.t(), out=c)
+        side.synchronize()
+        ev = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(len(work) + 1)]
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=side):
+            cs = torch.cuda.current_stream()
+            for i, (M, N, K, views) in enumerate(work):
+                ev[i].record(cs)
+                for a, b, c in views:
+                    torch.mm(a, b.t(), out=c)
+            ev[-1].record(cs)
+    stream.wait_stream(side)
+    g.replay()
+    torch.cuda.synchronize()
+    samples = []
+    for _ in range(steps):
+        g.replay()
+        torch.cuda.synchronize()
+        samples.append([ev[i].elapsed_time(ev[i + 1]) / R for i in range(len(work))])
+    per_pt = [statistics.median(s_[j] for s_ in samples) for j in range(len(work))]
+    del g, arenas
+    return per_pt
+
+
+def selector_overhead(vx, plans_nk, local):
+    """E6/E7 analogues: vx_plan build time and rung count per
+    (N,K), and host time of vx_plan_select over M = 1..16384 -- first call (memo miss,
+    the full Eq. 2-4 argmin) and repeated call (memo hit).  Measured through ctypes, so
+    each figure includes ~1 us of Python call overhead."""
+    import ctypes
+    out = {"plans": []}
+    c = vx.Choice()
+    for N, K in plans_nk:
+        t0 = time.perf_counter()
+        p = vx.Plan(N, K, "bf16", "bf16", "nk", device=local)
+        t_plan = time.perf_counter() - t0
+        h, f = p.handle, vx.lib.vx_plan_select
+        t0 = time.perf_counter()
+        for M in range(1, 16385):
+            f(h, 1, M, N, ctypes.byref(c))
+        t_cold = (time.perf_counter() - t0) / 16384
+        t0 = time.perf_counter()
+        for M in range(1, 16385):
+            f(h, 1, M, N, ctypes.byref(c))
+        t_warm = (time.perf_counter() - t0) / 16384
+        out["plans"].append({"N": N, "K": K, "rungs": len(p.dump()["rungs"]),
+                             "plan_ms": t_plan * 1e3, "select_us_first": t_cold * 1e6,
+                             "select_us_memo": t_warm * 1e6})
+    out["how"] = ("vx_plan wall time (no profiling: the calibration is compiled in); "
+                  "vx_plan_select per call via ctypes over M=1..16384, first pass (argmin) "
+                  "and second pass (memo)")
+    return out
 
 
 def run_sharded(args, rank, world, local, vx, stream, side, l2):
@@ -569,6 +660,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--points-out", default=None, help="write per-point results (json)")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-staged e2e leg")
+    ap.add_argument("--no-cublas", action="store_true",
+                    help="skip the informational cuBLAS line (torch.mm on the same points)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "mine":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

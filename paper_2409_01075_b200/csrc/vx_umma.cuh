@@ -504,6 +504,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             const bool tr = p.trace != nullptr;
             const uint32_t idesc = p.idesc;
             const bool mma_off = (p.dbg & 512) != 0;   // debug: TMA streaming only
+            // stage-0 operand descriptors; a stage / k-step only moves the 14-bit start
+            // address field (addr >> 4), so later descriptors are one 64-bit add away
+            const uint64_t dP_base = P_MN ? ptx::sdesc_mn_sw128(ptx::smem_addr(sP), 8192)
+                                          : ptx::sdesc_k_sw128(ptx::smem_addr(sP));
+            const uint64_t dQ_base = Q_MN ? ptx::sdesc_mn_sw128(ptx::smem_addr(sQ), 8192)
+                                          : ptx::sdesc_k_sw128(ptx::smem_addr(sQ));
+            constexpr uint32_t kStepP = P_MN ? (2048 >> 4) : (32 >> 4);   // per UMMA_K=16
+            constexpr uint32_t kStepQ = Q_MN ? (2048 >> 4) : (32 >> 4);
             int stage = 0;
             uint32_t phase = 0;
             int it = 0;
@@ -521,18 +529,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ptx::tc_fence_after();
                     const long long c1 = tr ? clock64() : 0;
                     if (it == 0 && i == 0 && lane == 0) trace_at(p, 3);
-                    const uint32_t aP = ptx::smem_addr(sP + stage * kP);
-                    const uint32_t aQ = ptx::smem_addr(sQ + stage * kQ);
+                    const uint64_t dp0 = dP_base + (uint64_t)(stage * (kP >> 4));
+                    const uint64_t dq0 = dQ_base + (uint64_t)(stage * (kQ >> 4));
                     long long c2 = 0;
                     if (ptx::elect_one()) {
                         if (!mma_off) {
 #pragma unroll
                             for (int k = 0; k < 4; ++k) {
                                 // K-major: +32 B inside the swizzle row; MN-major: +2 K-groups
-                                const uint64_t dp = P_MN ? ptx::sdesc_mn_sw128(aP + k * 2048, 8192)
-                                                         : ptx::sdesc_k_sw128(aP + k * 32);
-                                const uint64_t dq = Q_MN ? ptx::sdesc_mn_sw128(aQ + k * 2048, 8192)
-                                                         : ptx::sdesc_k_sw128(aQ + k * 32);
+                                const uint64_t dp = dp0 + k * kStepP;
+                                const uint64_t dq = dq0 + k * kStepQ;
                                 if (PAIR) ptx::umma_f16_pair(d_tmem, dp, dq, idesc, (i | k) != 0);
                                 else ptx::umma_f16(d_tmem, dp, dq, idesc, (i | k) != 0);
                             }

@@ -200,22 +200,35 @@ def fit(args):
     else:
         # greedy coordinate search on multiplicative steps: the regret objective is
         # piecewise constant, so move one log-parameter at a time while it helps
-        xb = list(x0)
-        fb = loss(np.array(xb))
         steps = [math.log(f) for f in (2.0, 1.4, 1.15, 1.05)]
-        for sweep in range(args.sweeps):
-            improved = False
-            for i in range(len(xb)):
-                for st in steps:
-                    for sg in (1, -1):
-                        xt = list(xb)
-                        xt[i] = min(max(xt[i] + sg * st, lo[i]), hi[i])
-                        ft = loss(np.array(xt))
-                        if ft < fb - 1e-9:
-                            xb, fb, improved = xt, ft, True
-            print("sweep %d objective %.5f" % (sweep, fb), flush=True)
-            if not improved:
-                break
+
+        def descend(x, f):
+            for sweep in range(args.sweeps):
+                improved = False
+                for i in range(len(x)):
+                    for st in steps:
+                        for sg in (1, -1):
+                            xt = list(x)
+                            xt[i] = min(max(xt[i] + sg * st, lo[i]), hi[i])
+                            ft = loss(np.array(xt))
+                            if ft < f - 1e-9:
+                                x, f, improved = xt, ft, True
+                print("sweep %d objective %.5f" % (sweep, f), flush=True)
+                if not improved:
+                    break
+            return x, f
+
+        xb = list(x0)
+        xb, fb = descend(xb, loss(np.array(xb)))
+        # random restarts around the incumbent (the regret objective is piecewise constant
+        # with many plateaus); seeded, so the fit is reproducible
+        rng = np.random.default_rng(args.seed)
+        for r in range(args.restarts):
+            xs = [min(max(v + rng.normal(0.0, 0.35), a), b) for v, a, b in zip(xb, lo, hi)]
+            xs, fs = descend(xs, loss(np.array(xs)))
+            print("restart %d objective %.5f (best %.5f)" % (r, fs, min(fs, fb)), flush=True)
+            if fs < fb:
+                xb, fb = xs, fs
 
         class R:
             pass
@@ -258,6 +271,8 @@ def main():
     f.add_argument("--method", default="coord", choices=["coord", "powell"])
     f.add_argument("--sweeps", type=int, default=12)
     f.add_argument("--err-weight", type=float, default=1.0)
+    f.add_argument("--restarts", type=int, default=0)
+    f.add_argument("--seed", type=int, default=0)
     args = ap.parse_args()
     if args.cmd == "measure":
         measure(args)
