@@ -70,7 +70,7 @@ class Choice(ctypes.Structure):
 
 def _load():
     if not os.path.exists(LIB_PATH):
-        raise ImportError("libvx.so not built: run `python -m paper_2409_01075_b200.build` "
+        raise ImportError("libvx.so not built: run `python __graft_entry__.py` "
                           "(no CPU fallback exists)")
     L = ctypes.CDLL(LIB_PATH)
     i64, i32, vp = ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p

@@ -1,6 +1,6 @@
 """Build libvx.so in-tree: nvcc for sm_100a only (tcgen05/TMA need the 'a' target).
 
-    python -m paper_2409_01075_b200.build [--verbose]
+    python paper_2409_01075_b200/build.py [--force] [--verbose]
 
 The shared object lands next to this file so it travels with the repo snapshot to the
 GPU box.  cudart is linked statically; the CUDA driver is reached through
