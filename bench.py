@@ -10,9 +10,9 @@ the SURVEY 8(d) d2 M sweeps (192 points), bf16 in / fp32 accumulate / bf16 out, 
 [N,K] weight.  One STEP = one vx_gemm call (selection + launch) per sweep point.
 
 Timing: one step = one CUDA graph holding, for each of the 192 points, an external event
-node and 8 back-to-back vx_gemm launches on fresh slices of >= 1 GiB operand arenas (cold
+node and R_PER_POINT = 48 back-to-back vx_gemm launches on fresh slices of >= 1 GiB operand arenas (cold
 L2: a slice is reused only after its arena wraps); selection + tensor maps run at capture.
-Per-launch time = (event[i+1] - event[i]) / 8, median over the K timed steps (max over
+Per-launch time = (event[i+1] - event[i]) / 48, median over the K timed steps (max over
 ranks for N > 1).  value = geomean over points of TFLOP/s (x N ranks: each rank
 runs its own copy of the sweep -> weak scaling; no data-path collective).  The M=65536
 LLaMA FFN of configs[4] is additionally run row-sharded across the N ranks ("sharded").
@@ -240,15 +240,18 @@ def workload_config():
             "points": len(sweep_points()), "in": "bf16", "out": "bf16", "accumulate": "fp32",
             "l2": "operands cold: every launch takes fresh slices of >= 1 GiB A/B/C arenas "
                   "(reuse only after the arena wraps, ~8x L2); one CUDA graph per step = "
-                  "192 points x 8 back-to-back launches, external event nodes between points; "
-                  "per-launch time = point interval / 8",
+                  "192 points x %d back-to-back launches, external event nodes between points; "
+                  "per-launch time = point interval / %d" % (R_PER_POINT, R_PER_POINT),
             "sharded": "configs[4]: M=65536, N=11008, K=4096 row-sharded over n_gpus"}
 
 
 # ----------------------------------------------------------------------------------------
 # the product arm
 # ----------------------------------------------------------------------------------------
-R_PER_POINT = 8
+# launches per sweep point: an event node between points costs ~10 us of drain (it breaks the
+# programmatic-dependent-launch overlap; tools/transition_probe.py), so R amortises it
+# (R = 50)
+R_PER_POINT = 48
 
 
 class Arena:

@@ -59,7 +59,8 @@ struct UmmaParams {
     unsigned long long* trace;  // optional per-CTA phase timestamps (VX_TRACE), else null
     int dbg;                    // debug bits (VX_DEBUG_FLAGS): 1 skip split push, 2 skip split
                                 // reduce, 4 skip split C store, 8 skip epilogue stores,
-                                // 32 skip stream-K fix-up (timing experiments only)
+                                // 32 skip stream-K fix-up, 1024 / 2048 operand loads
+                                // evict_first / evict_normal (timing experiments only)
     int streamk;                // 1: stream-K schedule over (tile, k-block) units
     int pair;                   // 1: cta_group::2 pair rung (cluster of 2, 256-row tiles)
     int bpack;                  // 1: B is VX_B_PACKED (5-D map of 64 x 64 contiguous tiles)
@@ -411,7 +412,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             // ===== TMA producers: producer `pid` takes this CTA's k-blocks j % 2 == pid =====
             const int pid = warp == 0 ? 0 : 1;
-            const uint64_t pol = ptx::policy_evict_last();
+            const long long cy0 = p.trace ? clock64() : 0;   // trace: setup -> first issue
+            const uint64_t pol = (p.dbg & 1024) ? ptx::policy_evict_first()
+                               : (p.dbg & 2048) ? ptx::policy_evict_normal()
+                                                : ptx::policy_evict_last();
             int stage = 0;
             uint32_t phase = 0;
             bool stamped = pid != 0;
@@ -453,6 +457,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                         if (++stage == S) { stage = 0; phase ^= 1; }
                         continue;
+                    }
+                    if (!stamped && kb == k0 && p.trace) {
+                        p.trace[blockIdx.x * kTraceSlots + 18] = clock64() - cy0;
                     }
                     ptx::mbar_arrive_expect_tx(&full[stage], kP + kQ);
                     if (!stamped && kb == k0) trace_at(p, 11);

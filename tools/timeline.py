@@ -94,6 +94,11 @@ def main():
         n = cy[:, 3].astype(float)
         print("  MMA issuer cycles per k-block: wait-full %.0f  issue %.0f  commit %.0f" % (
             np.median(cy[:, 0] / n), np.median(cy[:, 1] / n), np.median(cy[:, 2] / n)))
+    c18 = t[1:, :, 18].reshape(-1)
+    c18 = c18[c18 > 0]
+    if len(c18):
+        print("  producer cycles dep-wait -> first TMA issue: median %.0f  max %.0f" % (
+            np.median(c18), c18.max()))
     for nm in PH:
         if nm != "-" and rows[nm]:
             v = np.median(np.array(rows[nm]), axis=0)
