@@ -19,7 +19,7 @@
 namespace vx {
 
 static std::atomic<int64_t> g_launches{0};
-static unsigned long long* g_trace = nullptr;  // device buffer, 20 x u64 per CTA (debug)
+static unsigned long long* g_trace = nullptr;  // device buffer, 32 x u64 per CTA (debug)
 static const int g_dbg = [] {                 // VX_DEBUG_FLAGS (kernel phase skips, debug only)
     const char* e = getenv("VX_DEBUG_FLAGS");
     return e ? atoi(e) : 0;

@@ -138,7 +138,7 @@ __device__ __forceinline__ void epi_bar() {   // named barrier over the 8 epilog
     asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
 }
 
-constexpr int kTraceSlots = 20;
+constexpr int kTraceSlots = 32;
 // phase trace (tracing aux subsystem): %globaltimer (ns) at fixed points, 20 slots per CTA
 // (slots 12-15: MMA-issuer cycle counters, see the MMA loop)
 __device__ __forceinline__ void trace_at(const UmmaParams& p, int slot) {
@@ -147,6 +147,10 @@ __device__ __forceinline__ void trace_at(const UmmaParams& p, int slot) {
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         p.trace[blockIdx.x * kTraceSlots + slot] = t;
     }
+}
+// cycle-counter stamp (slots 18-31): clock64() - base
+__device__ __forceinline__ void cyc_at(const UmmaParams& p, int slot, long long base) {
+    if (p.trace) p.trace[blockIdx.x * kTraceSlots + slot] = clock64() - base;
 }
 
 constexpr int kGroupP = 16;   // raster: 16 P-tiles x all Q-tiles per group (L2 reuse)
@@ -339,6 +343,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int S = p.stages;
+    const long long cyc_entry = clock64();
     if (threadIdx.x == 0) trace_at(p, 0);
 
     // layout: [barriers | pad to 1024 | S x P tiles | S x Q tiles]
@@ -368,29 +373,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         ptx::mbar_init(redbar, 1);
         ptx::fence_mbar_init();
+        cyc_at(p, 24, cyc_entry);
     }
     if (warp == 1) {
+        const long long c = clock64();
         if (PAIR) ptx::tmem_alloc_pair<Cfg::kTmemCols>(tmem_holder);
         else ptx::tmem_alloc<Cfg::kTmemCols>(tmem_holder);
-    }
-    if (warp == 0 && lane == 0 && !(p.dbg & 128) && !p.bpack && !P_MN && !Q_MN) {
-        // L2 prefetch of this CTA's first ring-full of P and Q tiles, before the grid
-        // dependency wait: the first loads after it then hit L2 instead of DRAM
-        const int rk = p.splits > 1 ? (int)(blockIdx.x % p.splits) : 0;
-        const int pr = PAIR ? (int)ptx::cluster_ctarank() : 0;
-        WorkIter w0(p, rk);
-        int t, k0, nk;
-        if (w0.next(p, t, k0, nk)) {
-            int b, tp, tq;
-            decode_tile(t, p.tiles_p, p.tiles_q, b, tp, tq);
-            const int pp = PAIR ? tp * 256 + pr * 128 : tp * 128;
-            const int qq = PAIR ? tq * BN + pr * (BN / 2) : tq * BN;
-            const int n = nk < S ? nk : S;
-            for (int kb = k0; kb < k0 + n; ++kb) {
-                ptx::tma_prefetch_3d(&tmP, kb * 64, pp, b);
-                ptx::tma_prefetch_3d(&tmQ, kb * 64, qq, b);
-            }
-        }
+        if (lane == 0) cyc_at(p, 28, c);
     }
     ptx::tc_fence_before();
     if (PAIR) ptx::cluster_sync();   // both CTAs' barriers initialised before any remote use
@@ -398,11 +387,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::tc_fence_after();
     const uint32_t prank = PAIR ? ptx::cluster_ctarank() : 0;   // 0 = pair leader
     const uint32_t tmem_base = *tmem_holder;
-    if (threadIdx.x == 0) trace_at(p, 1);
-    // everything above (barrier init, TMEM alloc, descriptor prefetch) overlaps the previous
-    // kernel under PDL; no global memory is touched before this point
-    ptx::grid_dep_wait();
-    if (threadIdx.x == 0) trace_at(p, 8);
+    if (threadIdx.x == 0) { trace_at(p, 1); cyc_at(p, 26, cyc_entry); }
+    // Programmatic dependent launch: everything up to each role's first global access
+    // overlaps the previous kernel.  Each role waits for the previous grid right before it
+    // touches global memory: the producers after their first-tile bookkeeping and ring
+    // setup (so that code, cold in the instruction cache at every launch, runs before the
+    // wait, tools/timeline.py cycle stamps), the epilogue warps before anything else; the
+    // MMA warp never touches global memory.
 
     const bool split = p.splits > 1;
     const int rank = split ? (int)(blockIdx.x % p.splits) : 0;
@@ -416,27 +407,53 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t pol = (p.dbg & 1024) ? ptx::policy_evict_first()
                                : (p.dbg & 2048) ? ptx::policy_evict_normal()
                                                 : ptx::policy_evict_last();
+            if (pid == 0) cyc_at(p, 20, cy0);
             int stage = 0;
             uint32_t phase = 0;
             bool stamped = pid != 0;
+            bool waited = false;
             int j = 0;                       // running k-block count of this CTA
+            // first k-block of this producer: (pid 0) L2 prefetch of the CTA's first ring of
+            // P and Q tiles -- the loads after the wait then hit L2 -- then the grid
+            // dependency wait (no global memory is touched before it)
+            auto dep_wait = [&](int tile_, int kb_, int nleft) {
+                if (waited) return;
+                if (pid == 0 && !(p.dbg & 128) && !p.bpack && !P_MN && !Q_MN) {
+                    int b_, tp_, tq_;
+                    decode_tile(tile_, p.tiles_p, p.tiles_q, b_, tp_, tq_);
+                    const int pp = PAIR ? tp_ * 256 + (int)prank * 128 : tp_ * 128;
+                    const int qq = PAIR ? tq_ * BN + (int)prank * (BN / 2) : tq_ * BN;
+                    const int n = nleft < S ? nleft : S;
+                    for (int kb2 = kb_; kb2 < kb_ + n; ++kb2) {
+                        ptx::tma_prefetch_3d(&tmP, kb2 * 64, pp, b_);
+                        ptx::tma_prefetch_3d(&tmQ, kb2 * 64, qq, b_);
+                    }
+                }
+                ptx::grid_dep_wait();
+                waited = true;
+                if (pid == 0) { trace_at(p, 8); cyc_at(p, 27, cyc_entry); }
+            };
             WorkIter wi(p, rank);
+            if (pid == 0) cyc_at(p, 21, cy0);
             int tile, k0, nk;
             while (wi.next(p, tile, k0, nk)) {
                 int b, tp, tq;
                 decode_tile(tile, p.tiles_p, p.tiles_q, b, tp, tq);
+                if (pid == 0 && j == 0) cyc_at(p, 22, cy0);
                 for (int kb = k0; kb < k0 + nk; ++kb, ++j) {
                     if (j % kProdWarps != pid) {
                         if (++stage == S) { stage = 0; phase ^= 1; }
                         continue;
                     }
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
+                    if (j == 0) cyc_at(p, 23, cy0);
                     if (kb >= k0 + kProdWarps && !stamped) { trace_at(p, 10); stamped = true; }
                     uint8_t* dP = sP + stage * kP;
                     uint8_t* dQ = sQ + stage * kQ;
                     if (PAIR) {
                         // both halves complete on the leader's full barrier
                         if (prank == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2 * (kP + kQ));
+                        dep_wait(tile, kb, k0 + nk - kb);
                         ptx::tma_load_3d_pair(dP, &tmP, &full[stage], kb * 64,
                                               tp * 256 + (int)prank * 128, b, pol);
                         if (p.bpack) {             // this CTA's BN/2 rows = BN/128 packed tiles
@@ -462,6 +479,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         p.trace[blockIdx.x * kTraceSlots + 18] = clock64() - cy0;
                     }
                     ptx::mbar_arrive_expect_tx(&full[stage], kP + kQ);
+                    dep_wait(tile, kb, k0 + nk - kb);
                     if (!stamped && kb == k0) trace_at(p, 11);
                     if (p.bpack) {
                         // B pre-packed: every 64-row block of the B tile is one 8-KB box
@@ -581,6 +599,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (is_epi_warp(warp)) {
         // ===== epilogue warps =====
+        ptx::grid_dep_wait();
         // warp w reads TMEM lanes 32*(w%4)..+31 (its quarter of the tile rows); the two
         // warps of a quarter (group g = 0, 1) take alternate column chunks
         const int quarter = warp & 3;
@@ -606,7 +625,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t acc_phase = (it >> 1) & 1;
             ptx::mbar_wait(&tfull[acc], acc_phase);
             ptx::tc_fence_after();
-            if (it == 0 && threadIdx.x == kEpiWarp0 * 32) trace_at(p, 5);
+            const bool st0 = it == 0 && threadIdx.x == kEpiWarp0 * 32;
+            const long long cye = st0 ? clock64() : 0;
+            if (st0) trace_at(p, 5);
             const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
             if (split) break;  // split mode: the accumulator is read after the cluster barrier
             // ---- stream-K: a cut tile ----------------------------------------------------
@@ -685,6 +706,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             ptx::tmem_ld32(taddr + k * CW + 32,
                                            *reinterpret_cast<uint32_t(*)[32]>(v + 32));
                             ptx::tmem_wait_ld();
+                            if (st0 && k == grp) cyc_at(p, 29, cye);
                             add_partials<64, PAIR>(v, p.ws, c_first, c_last, row, k * CW, BN, prank);
                             uint32_t u[32];
                             pack_chunk<64>(reinterpret_cast<const float*>(v), u, p.out_kind);
@@ -739,6 +761,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         pending = true;
                     }
                 }
+                if (st0) cyc_at(p, 30, cye);
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) release_acc(&tempty[acc]);
@@ -779,10 +802,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         // TMA stores have read their staging before the CTA retires (the grid completes only
         // once the stores are performed, which is what the next grid's wait observes)
+        const long long cyw = clock64();
         if (lane == 0) {
             if (p.dbg & 256) ptx::bulk_wait<0>();
             else ptx::bulk_wait_read<0>();
         }
+        if (threadIdx.x == kEpiWarp0 * 32) cyc_at(p, 31, cyw);
     }
 
     __syncwarp();  // reconverge the single-lane roles before the .aligned cluster barriers

@@ -19,8 +19,8 @@ import paper_2409_01075_b200 as vx
 import synth
 
 PH = ["entry", "setup", "prod_done", "first_full", "mma_done", "acc_ready", "epi_done",
-      "pre_teardown", "dep_released", "exit", "2nd_issue", "1st_issue", "-", "-", "-", "-", "split_sync1", "split_posted", "-", "-"]
-NS = 20   # slots per CTA; 12-15 = MMA-issuer cycle counters (wait, issue, commit, n)
+      "pre_teardown", "dep_released", "exit", "2nd_issue", "1st_issue", "-", "-", "-", "-", "split_sync1", "split_posted", "-", "-"] + ["-"] * 12
+NS = 32   # slots per CTA; 12-15 = MMA-issuer cycle counters (wait, issue, commit, n), 18-31 cycle stamps
 
 
 def main():
@@ -94,11 +94,16 @@ def main():
         n = cy[:, 3].astype(float)
         print("  MMA issuer cycles per k-block: wait-full %.0f  issue %.0f  commit %.0f" % (
             np.median(cy[:, 0] / n), np.median(cy[:, 1] / n), np.median(cy[:, 2] / n)))
-    c18 = t[1:, :, 18].reshape(-1)
-    c18 = c18[c18 > 0]
-    if len(c18):
-        print("  producer cycles dep-wait -> first TMA issue: median %.0f  max %.0f" % (
-            np.median(c18), c18.max()))
+    CY = {18: "prod: dep-wait -> 1st issue", 20: "prod: createpolicy", 21: "prod: WorkIter",
+          22: "prod: next+decode", 23: "prod: 1st empty wait", 24: "setup: bar init (entry+)",
+          25: "setup: L2 prefetch (entry+)", 26: "setup: synced (entry+)",
+          27: "setup: dep released (entry+)", 28: "tmem alloc", 29: "epi: 1st tmem ld",
+          30: "epi: chunks issued", 31: "epi: bulk wait read"}
+    for sl, nm in CY.items():
+        c = t[1:, :, sl].reshape(-1)
+        c = c[c > 0]
+        if len(c):
+            print("  cyc %-30s median %7.0f  max %7.0f" % (nm, np.median(c), c.max()))
     for nm in PH:
         if nm != "-" and rows[nm]:
             v = np.median(np.array(rows[nm]), axis=0)
