@@ -22,26 +22,26 @@
 namespace vx {
 
 static const Calib kCalib = {
-    /*hbm_milli=*/3329822,   // 6543 GB/s measured copy bandwidth / 1.965 GHz
+    /*hbm_milli=*/3335674,   // 6543 GB/s measured copy bandwidth / 1.965 GHz
     /*dsm_milli=*/2931,      // effective in-cluster reduce rate (fitted)
-    /*fixed_cluster=*/2152,  // cluster launch + two cluster barriers (fitted)
-    /*skfix_milli=*/9589,   // stream-K partial write + read-back (fitted)
+    /*fixed_cluster=*/249,  // cluster launch + two cluster barriers (fitted)
+    /*skfix_milli=*/19022,   // stream-K partial write + read-back (fitted)
 };
 
 static const RungCalib kRungs[] = {
-    {"umma_128x64", 1000367, 44315, 8000, 6967},
-    {"umma_128x128", 1442773, 72562, 48886, 747},
-    {"umma_128x256", 1672861, 160000, 512000, 500},
-    {"umma_256x128", 3140267, 160000, 122563, 5546},
-    {"umma_256x256", 4096000, 126195, 174150, 525},
-    {"umma_swap_128x16", 1000000, 17920, 8000, 3524},
-    {"umma_swap_128x32", 1000000, 28993, 8000, 3550},
-    {"umma_swap_128x64", 1000000, 46161, 512000, 7856},
-    {"umma_swap_128x128", 1449009, 69107, 48979, 1975},
-    {"gemv_1x8", 4328, 63578, 4000, 2628},
+    {"umma_128x64", 1000367, 44315, 8000, 9214},
+    {"umma_128x128", 1442773, 160000, 16764, 1203},
+    {"umma_128x256", 1672861, 84000, 512000, 500},
+    {"umma_256x128", 3140267, 160000, 120112, 4367},
+    {"umma_256x256", 4096000, 152381, 512000, 500},
+    {"umma_swap_128x16", 1000000, 20745, 8000, 4053},
+    {"umma_swap_128x32", 1000000, 28993, 8000, 4315},
+    {"umma_swap_128x64", 1000000, 42147, 512000, 5892},
+    {"umma_swap_128x128", 1449009, 160000, 17139, 1411},
+    {"gemv_1x8", 4328, 63578, 16000, 2628},
     {"gemv_2x8", 8000, 74202, 1000, 3062},
-    {"gemv_4x8", 8000, 64524, 1000, 1997},
-    {"gemv_8x8", 13818, 6491, 1000, 326},
+    {"gemv_4x8", 8762, 64524, 1000, 2312},
+    {"gemv_8x8", 8832, 5888, 2000, 200},
     {"simt_32x32", 128000, 32000, 16000, 2000},
     {"simt_64x64", 128000, 32000, 16000, 2000},
     {"simt_128x64", 128000, 32000, 16000, 2000},

@@ -335,3 +335,36 @@ def test_gemv_rungs_tiny_m(bl, out):
     Q, Kt = synth.gemm_inputs(3, 40, 64, "bf16", "nk", kind="int", seed=9, batch=5)
     got, _ = _run(pb, Q, Kt, force=(g["rung_id"], 1))
     assert np.array_equal(got, oracle.gemm(Q, Kt, "nk"))
+
+
+def test_chained_launches_pdl_dependency():
+    """Programmatic dependent launch: each role waits for the previous grid
+    only at its first global access.  A chain of launches on one stream, ping-ponging two
+    activation buffers (launch i reads what launch i-1 wrote: RAW; and overwrites what
+    launch i-1 read: WAR), with B a permutation matrix so every step is exact:
+    X_{i+1}[m, n] = X_i[m, perm[n]].  Every rung x split, no synchronisation inside the
+    chain, stream-K flags reused across launches."""
+    vx = vxmod()
+    N = K = 384
+    rng = np.random.default_rng(7)
+    perm = rng.permutation(K)
+    Bp = np.zeros((N, K), dtype=np.float32)
+    Bp[np.arange(N), perm] = 1.0
+    B = torch.from_numpy(Bp).to(torch.bfloat16).cuda()
+    p = vx.Plan(N, K, "bf16", "bf16", "nk")
+    L = 6
+    for M in (5, 129, 333):
+        A0, _ = synth.gemm_inputs(M, N, K, "bf16", "nk", kind="int", seed=300 + M)
+        want = A0.double().numpy()
+        for _ in range(L):
+            want = want[:, perm]
+        for r in p.dump()["rungs"]:
+            if not _ok(r, M):
+                continue
+            for s in r["splits"]:
+                X = [A0.cuda(), torch.empty((M, K), dtype=torch.bfloat16, device="cuda")]
+                for i in range(L):
+                    p.gemm(X[i % 2], B, out=X[(i + 1) % 2], force=(r["rung_id"], s))
+                torch.cuda.synchronize()
+                got = X[L % 2].cpu().double().numpy()
+                assert np.array_equal(got, want), (M, r, s)

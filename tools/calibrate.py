@@ -21,10 +21,13 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-CAL_M = (1, 2, 4, 8, 16, 32, 64, 128, 200, 384, 512, 768, 1024, 1536, 2048, 3072, 4096, 8192)
-# generic (N, K): powers of two and N with odd tile counts (13 / 21 / 42 tiles of 256)
+CAL_M = (1, 2, 4, 8, 16, 24, 32, 48, 64, 96, 128, 160, 200, 256, 320, 384, 512, 768, 1024, 1536,
+         2048, 3072, 4096, 8192)
+# generic (N, K): powers of two and N with odd tile counts (13 / 21 / 42 tiles of 256), plus
+# small-K shapes (K <= 1024: few k-blocks, the launch-floor regime) with odd tile counts
 CAL_NK = ((1024, 1024), (4096, 1024), (2048, 4096), (8192, 4096), (6144, 2048),
-          (3328, 1536), (5376, 4096), (10752, 2048), (1536, 512), (2560, 640))
+          (3328, 1536), (5376, 4096), (10752, 2048), (1536, 512), (2560, 640),
+          (1280, 896), (3584, 640), (2048, 512))
 CLOCK_GHZ = 1.965   # cycles of the model are SM cycles at the max clock
 
 
@@ -259,6 +262,43 @@ def fit(args):
     print(json.dumps(out, indent=1))
 
 
+def heldout(args):
+    """Selector regret on benchmark shapes NOT used by the fit (tools/sweep.py --shapes all
+    output), for one or more calibration files (oracle/calib_b200.json format)."""
+    import paper_2409_01075_b200 as vx
+    raw = json.load(open(args.raw))             # calibration raw data: only its descriptor
+    desc = raw["desc"]
+    dd = vx.DeviceDesc.from_json(desc)
+    sw = json.load(open(args.sweep))
+    fam = {0: "umma", 1: "umma_swap", 3: "gemv"}
+    for cf in args.calib:
+        cal = json.load(open(cf))
+        th = {n: dict(mac=r["mac_milli"] / 1000, l2s=r["l2s_milli"] / 1000, epi=r["epi_milli"] / 1000,
+                      fixed=r["fixed"]) for n, r in cal["rungs"].items()}
+        g = dict(hbm=cal["hbm_milli"] / 1000, dsm=cal["dsm_milli"] / 1000,
+                 fixed_cluster=cal["fixed_cluster"], skfix=cal["skfix_milli"] / 1000)
+        plans, regs, by = {}, [], {}
+        for e in sw:
+            if e.get("batch", 1) != 1:
+                continue
+            N, K, M = e["N"], e["K"], e["M"]
+            if (N, K) not in plans:
+                plans[(N, K)] = {r["rung_id"]: r for r in vx.Plan(N, K, "bf16", "bf16", "nk", desc=dd).dump()["rungs"]}
+            rt = plans[(N, K)]
+            best = min(f["us"] for f in e["forced"])
+            def pred(f):
+                r = rt[f["rung"]]
+                sm = dict(M=M, N=N, K=K, split=f["split"], family=r["family"], bm=r["bm"], bn=r["bn"])
+                return model_us(sm, th["%s_%dx%d" % (fam[r["family"]], r["bm"], r["bn"])], desc, g)
+            pick = min(e["forced"], key=pred)
+            regs.append(best / pick["us"])
+            tag = "bert" if K == 768 else "llama"
+            by.setdefault(tag, []).append(best / pick["us"])
+        gm = lambda v: math.exp(sum(math.log(x) for x in v) / len(v))
+        print("%s: held-out regret geomean %.4f worst %.4f  (%s)" % (
+            cf, gm(regs), min(regs), ", ".join("%s %.4f" % (k, gm(v)) for k, v in sorted(by.items()))))
+
+
 def main():
     ap = argparse.ArgumentParser()
     sub = ap.add_subparsers(dest="cmd")
@@ -273,9 +313,15 @@ def main():
     f.add_argument("--err-weight", type=float, default=1.0)
     f.add_argument("--restarts", type=int, default=0)
     f.add_argument("--seed", type=int, default=0)
+    h = sub.add_parser("heldout")
+    h.add_argument("raw")
+    h.add_argument("sweep")
+    h.add_argument("calib", nargs="+")
     args = ap.parse_args()
     if args.cmd == "measure":
         measure(args)
+    elif args.cmd == "heldout":
+        heldout(args)
     else:
         fit(args)
 
