@@ -377,14 +377,19 @@ def _streamk_cost(rung, batch, M, N, K, mt, nt, tm, tn, tiles, kb, in_b, out_b, 
 SK_MAX_WAVES = 3
 
 
-def streamk_admissible(rung: dict, batch: int, M: int, N: int, desc: dict) -> bool:
+def streamk_admissible(rung: dict, batch: int, M: int, N: int, K: int, desc: dict) -> bool:
     """R19: stream-K competes only where the rung's data-parallel schedule needs at most
-    SK_MAX_WAVES waves, i.e. where wave quantization is what it removes."""
+    SK_MAX_WAVES waves, i.e. where wave quantization is what it removes, and where every
+    CTA's share of the units is at least half a tile's K loop (2 * ceil(U/G) >= k-blocks),
+    so a cut tile gathers partials from at most a few CTAs."""
     mt, nt = (N, M) if rung["swap"] else (M, N)
     tiles = batch * ceil_div(mt, rung["bm"]) * ceil_div(nt, rung["bn"])
     cg = rung["cg"]
     slots = desc["max_active_clusters"][str(cg)] * cg
-    return tiles * cg <= SK_MAX_WAVES * slots
+    kb = ceil_div(K, rung["bk"])
+    U = tiles * kb
+    G = min(desc["max_active_clusters"][str(cg)], U)
+    return tiles * cg <= SK_MAX_WAVES * slots and 2 * ceil_div(U, G) >= kb
 
 
 def select(table: dict, batch: int, M: int, N: int, K: int, desc: dict, calib: dict) -> dict:
@@ -393,7 +398,7 @@ def select(table: dict, batch: int, M: int, N: int, K: int, desc: dict, calib: d
     best = None
     for r in table["rungs"]:
         for s in r["splits"]:
-            if s == 0 and not streamk_admissible(r, batch, M, N, desc):
+            if s == 0 and not streamk_admissible(r, batch, M, N, K, desc):
                 continue
             if r["family"] == 3 and M > r["bm"]:      # GEMV rungs hold M <= MT rows (R20)
                 continue

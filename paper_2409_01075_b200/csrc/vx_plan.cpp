@@ -203,13 +203,18 @@ static vx_status build_rungs(vx_plan_s* p) {
 }
 
 // stream-K is admitted only where wave quantization is what it fixes: the data-parallel
-// schedule of the rung needs at most kSkMaxWaves waves (R19)
+// schedule of the rung needs at most kSkMaxWaves waves; and only where every CTA's share of
+// the units is at least half a tile's K loop, so a cut tile gathers few partials (R19)
 constexpr int64_t kSkMaxWaves = 3;
 static bool sk_admissible(const vx_plan_s* p, const Rung& r, int64_t batch, int64_t M, int64_t N) {
     const int64_t mt = r.swap ? N : M, nt = r.swap ? M : N;
     const int64_t tiles = batch * cdiv(mt, r.bm) * cdiv(nt, r.bn);
-    const int64_t slots = (int64_t)p->desc.max_active_clusters[r.cg == 2 ? 1 : 0] * r.cg;
-    return tiles * r.cg <= kSkMaxWaves * slots;
+    const int64_t act = (int64_t)p->desc.max_active_clusters[r.cg == 2 ? 1 : 0];
+    const int64_t slots = act * r.cg;
+    const int64_t kb = cdiv(p->K, r.bk);
+    const int64_t U = tiles * kb;
+    const int64_t G = act < U ? act : U;
+    return tiles * r.cg <= kSkMaxWaves * slots && 2 * cdiv(U, G) >= kb;
 }
 
 // ---- runtime cost ----------------------------------------------------------

@@ -113,7 +113,7 @@ def _brute_best(t, batch, M, N, K):
     allc = []
     for r in t["rungs"]:
         for s in r["splits"]:
-            if s == 0 and not S.streamk_admissible(r, batch, M, N, DESC):   # R19
+            if s == 0 and not S.streamk_admissible(r, batch, M, N, K, DESC):   # R19
                 continue
             if r["family"] == 3 and M > r["bm"]:                            # R20
                 continue
@@ -182,7 +182,11 @@ def test_streamk_only_for_few_waves():
         ch = S.select(t, 1, M, 11008, 4096, DESC, CAL)
         if ch["split"] == 0:
             r = t["rungs"][ch["rung_id"]]
-            assert S.streamk_admissible(r, 1, M, 11008, DESC)
+            assert S.streamk_admissible(r, 1, M, 11008, 4096, DESC)
     big = [r for r in t["rungs"] if r["cg"] == 2 and r["family"] == 0][0]
-    assert not S.streamk_admissible(big, 1, 16384, 11008, DESC)
-    assert S.streamk_admissible(big, 1, 512, 11008, DESC)
+    assert not S.streamk_admissible(big, 1, 16384, 11008, 4096, DESC)
+    assert S.streamk_admissible(big, 1, 512, 11008, 4096, DESC)
+    # few k-blocks per CTA (BERT-size K, many small tiles): a tile would be cut over > 3 CTAs
+    sw16 = [r for r in t["rungs"] if r["family"] == 1 and r["bn"] == 16][0]
+    assert not S.streamk_admissible(sw16, 1, 32, 2304, 768, DESC)
+    assert S.streamk_admissible(sw16, 1, 4, 11008, 4096, DESC)

@@ -99,6 +99,8 @@ def model_us(sm, th, desc, g):
         U = tiles * kb
         G = min(desc["max_active_clusters"]["2" if bm == 256 else "1"], U)
         units = _cd(U, G)
+        if 2 * units < kb:      # R19: a CTA's share must be >= half a tile's K loop
+            return float("inf")
         segs = _cd(units, kb) + 1
         l = max(ls, t(2 * K * (mt + nt), units * hbm))
         tm_ = l + (units - 1) * max(l, c) + c
