@@ -393,7 +393,7 @@ def run_mine(args, rank, world, local):
                      algo_bytes(M, N, K) / (peaks["hbm_gbs"] * 1e9))
         frac = t_roof / (ms * 1e-3)
         if M >= 512:
-            bins_tc.append(tf / world / peaks["bf16_tflops"])
+            bins_tc.append(tf / world / peaks["bf16_tflops_sustained"])
         if M <= 64:
             bins_hbm.append(gbs / world / peaks["hbm_gbs"])
         rows.append({"tag": tag, "M": M, "N": N, "K": K, "us": ms * 1e3, "tflops": tf,
@@ -407,9 +407,13 @@ def run_mine(args, rank, world, local):
     dom_bytes = algo_bytes(dom["M"], dom["N"], dom["K"])
     tensor_bound = dom_flops / (peaks["bf16_tflops"] * 1e12) >= dom_bytes / (peaks["hbm_gbs"] * 1e9)
     if tensor_bound:
+        # the dominant kernel is timed inside a long step (the whole sweep graph, ~0.7 s of
+        # back-to-back GEMMs at the power cap): its denominator is the SUSTAINED measured
+        # peak (B200_PROFILING.md); the burst-peak fraction is reported beside it
         ach = dom_flops / (dom["us"] * 1e-6) / 1e12
-        roof = {"bound": "tensor", "achieved": ach, "peak": peaks["bf16_tflops"],
-                "unit": "TFLOP/s", "frac": ach / peaks["bf16_tflops"]}
+        pk = peaks["bf16_tflops_sustained"]
+        roof = {"bound": "tensor", "achieved": ach, "peak": pk, "unit": "TFLOP/s",
+                "frac": ach / pk, "frac_of_burst_peak": ach / peaks["bf16_tflops"]}
     else:
         ach = dom_bytes / (dom["us"] * 1e-6) / 1e9
         roof = {"bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
@@ -419,7 +423,7 @@ def run_mine(args, rank, world, local):
         dom["M"], dom["N"], dom["K"], dom["rung"], dom["split"])
     roof["share_of_step"] = dom["us"] * dom["R"] / (wall_ms / args.steps) / 1e3
     roof["launches_per_step"] = dom["R"]
-    roof["peak_source"] = peaks["source"] + " burst"
+    roof["peak_source"] = peaks["source"] + (" sustained" if tensor_bound else "")
 
     sharded = run_sharded(args, rank, world, local, vx, stream, side, l2)
     e2e = None if args.no_e2e else run_e2e(args, rank, world, local, vx, plans, pts, stream)
@@ -459,8 +463,12 @@ def run_mine(args, rank, world, local):
             "roofline": roof,
             "bins": {"tensor_frac_geomean_M>=512": geomean(bins_tc) if bins_tc else None,
                      "tensor_frac_geomean_M>=512_llama": geomean(
+                         [r["tflops"] / world / peaks["bf16_tflops_sustained"] for r in rows
+                          if r["M"] >= 512 and r["tag"] == "llama"]),
+                     "tensor_frac_geomean_M>=512_llama_vs_burst_peak": geomean(
                          [r["tflops"] / world / peaks["bf16_tflops"] for r in rows
                           if r["M"] >= 512 and r["tag"] == "llama"]),
+                     "tensor_peak_used": "bf16_tflops_sustained (the sweep is one long step)",
                      "hbm_frac_geomean_M<=64": geomean(bins_hbm) if bins_hbm else None,
                      "hbm_frac_geomean_M<=64_llama": geomean(
                          [r["gbs"] / world / peaks["hbm_gbs"] for r in rows
@@ -649,7 +657,14 @@ def load_traffic(dom):
         return None
     d = json.load(open(p))
     key = "%d_%d_%d" % (dom["M"], dom["N"], dom["K"])
-    return d.get(key)
+    if key in d:
+        return d[key]
+    # the same (N, K) captured at an M within 0.1% (e.g. 16384 for a dominant M = 16383)
+    for k, v in d.items():
+        m, n, kk = (int(x) for x in k.split("_"))
+        if n == dom["N"] and kk == dom["K"] and abs(m - dom["M"]) <= 0.001 * dom["M"]:
+            return v
+    return None
 
 
 def main():

@@ -24,24 +24,24 @@ namespace vx {
 static const Calib kCalib = {
     /*hbm_milli=*/3335674,   // 6543 GB/s measured copy bandwidth / 1.965 GHz
     /*dsm_milli=*/2931,      // effective in-cluster reduce rate (fitted)
-    /*fixed_cluster=*/249,  // cluster launch + two cluster barriers (fitted)
+    /*fixed_cluster=*/206,  // cluster launch + two cluster barriers (fitted)
     /*skfix_milli=*/19022,   // stream-K partial write + read-back (fitted)
 };
 
 static const RungCalib kRungs[] = {
-    {"umma_128x64", 1000367, 44315, 8000, 9214},
-    {"umma_128x128", 1442773, 160000, 16764, 1203},
+    {"umma_128x64", 1000367, 44315, 8000, 7631},
+    {"umma_128x128", 1442773, 145125, 16764, 1203},
     {"umma_128x256", 1672861, 84000, 512000, 500},
-    {"umma_256x128", 3140267, 160000, 120112, 4367},
-    {"umma_256x256", 4096000, 152381, 512000, 500},
+    {"umma_256x128", 3297280, 160000, 33559, 5273},
+    {"umma_256x256", 4096000, 152381, 72112, 500},
     {"umma_swap_128x16", 1000000, 20745, 8000, 4053},
-    {"umma_swap_128x32", 1000000, 28993, 8000, 4315},
+    {"umma_swap_128x32", 1000000, 28993, 8000, 4531},
     {"umma_swap_128x64", 1000000, 42147, 512000, 5892},
-    {"umma_swap_128x128", 1449009, 160000, 17139, 1411},
+    {"umma_swap_128x128", 1449009, 160000, 8000, 726},
     {"gemv_1x8", 4328, 63578, 16000, 2628},
     {"gemv_2x8", 8000, 74202, 1000, 3062},
-    {"gemv_4x8", 8762, 64524, 1000, 2312},
-    {"gemv_8x8", 8832, 5888, 2000, 200},
+    {"gemv_4x8", 8762, 64524, 1000, 2428},
+    {"gemv_8x8", 8832, 5888, 1217, 200},
     {"simt_32x32", 128000, 32000, 16000, 2000},
     {"simt_64x64", 128000, 32000, 16000, 2000},
     {"simt_128x64", 128000, 32000, 16000, 2000},

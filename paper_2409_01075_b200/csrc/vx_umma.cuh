@@ -621,6 +621,30 @@ __global__ void __launch_bounds__(kThreads, 1)
             decode_tile(tile, p.tiles_p, p.tiles_q, b, tp, tq);
             // first P-axis row of this CTA's accumulator rows (a pair splits 256 rows)
             const int prow0 = PAIR ? tp * 256 + (int)prank * 128 : tp * 128;
+            // ---- stream-K bookkeeping (before the accumulator wait) ---------------------
+            int c_first = 0, c_last = -1;          // CTAs whose partials this CTA adds
+            // stream-K ids: CTAs, or pairs (each CTA of a pair fixes up its own 128 rows)
+            const int sk_id = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+            const int sk_G = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+            if (p.streamk && k0 == 0 && nk < p.kb_total && !(p.dbg & 32)) {
+                // owner of a cut tile: the rest of its K range sits in ids sk_id+1 .. c_last.
+                // The contributors published their partials at the START of their ranges,
+                // so the flags are acquired here, while this tile's mainloop still runs --
+                // the atomic poll and fence stay off the tail of the launch.
+                c_first = sk_id + 1;
+                const long long last_unit = (long long)(tile + 1) * p.kb_total - 1;
+                c_last = sk_id;
+                while (c_last + 1 < sk_G && sk_first(c_last + 1, U, sk_G) <= last_unit) ++c_last;
+                // one thread acquires the contributors' flags (backing off between polls so
+                // the publishers' stores are not starved); the named barrier then orders
+                // every epilogue thread's partial reads after that acquire
+                if (threadIdx.x == kEpiWarp0 * 32) {
+                    for (int j = c_first; j <= c_last; ++j)
+                        while (atomicAdd(p.flags + sk_slot<PAIR>(j, prank), 0) == 0) __nanosleep(64);
+                    __threadfence();
+                }
+                epi_bar();
+            }
             const int acc = it & 1;
             const uint32_t acc_phase = (it >> 1) & 1;
             ptx::mbar_wait(&tfull[acc], acc_phase);
@@ -631,10 +655,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
             if (split) break;  // split mode: the accumulator is read after the cluster barrier
             // ---- stream-K: a cut tile ----------------------------------------------------
-            int c_first = 0, c_last = -1;          // CTAs whose partials this CTA adds
-            // stream-K ids: CTAs, or pairs (each CTA of a pair fixes up its own 128 rows)
-            const int sk_id = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
-            const int sk_G = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
             if (p.streamk && k0 > 0 && !(p.dbg & 32)) {
                 // not the owner: park the fp32 partial in this CTA's slot and publish it
                 // slot layout [col/4][row][4] (coalesced across the warp's rows)
@@ -661,22 +681,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                     atomicExch(p.flags + blockIdx.x, 1);
                 }
                 continue;
-            }
-            if (p.streamk && nk < p.kb_total && !(p.dbg & 32)) {
-                // owner of a cut tile: the rest of its K range sits in ids sk_id+1 .. c_last
-                c_first = sk_id + 1;
-                const long long last_unit = (long long)(tile + 1) * p.kb_total - 1;
-                c_last = sk_id;
-                while (c_last + 1 < sk_G && sk_first(c_last + 1, U, sk_G) <= last_unit) ++c_last;
-                // one thread acquires the contributors' flags (backing off between polls so
-                // the publishers' stores are not starved); the named barrier then orders
-                // every epilogue thread's partial reads after that acquire
-                if (threadIdx.x == kEpiWarp0 * 32) {
-                    for (int j = c_first; j <= c_last; ++j)
-                        while (atomicAdd(p.flags + sk_slot<PAIR>(j, prank), 0) == 0) __nanosleep(64);
-                    __threadfence();
-                }
-                epi_bar();
             }
             if (p.vec && !(p.dbg & 8)) {
                 // TMEM -> registers -> swizzled SMEM staging -> TMA bulk store (full lines,

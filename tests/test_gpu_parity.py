@@ -368,3 +368,19 @@ def test_chained_launches_pdl_dependency():
                 torch.cuda.synchronize()
                 got = X[L % 2].cpu().double().numpy()
                 assert np.array_equal(got, want), (M, r, s)
+
+
+def test_gemv_column_tail_nk():
+    """GEMV rungs (R20) own 8 columns per CTA (4 per warp): N = 394 leaves a 2-column tail
+    CTA with one warp group that has no columns; integer-exact for every MT."""
+    vx = vxmod()
+    N, K = 394, 1048
+    p = vx.Plan(N, K, "bf16", "fp32", "nk")
+    rungs = [r for r in p.dump()["rungs"] if r["family"] == 3]
+    for M in (1, 3, 8):
+        A, B = synth.gemm_inputs(M, N, K, "bf16", "nk", kind="int", seed=70 + M)
+        want = oracle.gemm(A, B, "nk")
+        for r in rungs:
+            if M <= r["bm"]:
+                got, _ = _run(p, A, B, force=(r["rung_id"], 1))
+                assert np.array_equal(got, want), (M, r["bm"])
