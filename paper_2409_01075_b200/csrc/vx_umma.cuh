@@ -816,6 +816,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     __syncwarp();  // reconverge the single-lane roles before the .aligned cluster barriers
     if (!split && threadIdx.x == kEpiWarp0 * 32) trace_at(p, 6);
+    long long cyr = 0;   // trace: start of the split reduce
     if (split) {
         // deterministic in-cluster reduce-scatter of the s K-slice partials (R7):
         //  (1) the owner thread of each CTA posts the byte count it expects from its peers
@@ -841,6 +842,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::cluster_sync();
         ptx::tc_fence_after();
         if (threadIdx.x == kEpiWarp0 * 32) trace_at(p, 16);
+        const long long cyp = clock64();
         if (is_epi_warp(warp) && post) {
             const int quarter = warp & 3;
             const int row = quarter * 32 + lane;
@@ -867,12 +869,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
         }
-        if (threadIdx.x == kEpiWarp0 * 32) trace_at(p, 17);
+        if (threadIdx.x == kEpiWarp0 * 32) { trace_at(p, 17); cyc_at(p, 30, cyp); }
         if (is_epi_warp(warp)) {
             epi_bar();                               // this CTA's own rows are in SMEM
+            if (threadIdx.x == kEpiWarp0 * 32) cyc_at(p, 19, cyp);
             if (post) ptx::mbar_wait(redbar, 0);     // the peers' rows too
         }
         if (threadIdx.x == kEpiWarp0 * 32) trace_at(p, 6);
+        cyr = clock64();
         if (is_epi_warp(warp) && !(p.dbg & 2)) {
             int b, tp, tq;
             decode_tile(tile0, p.tiles_p, p.tiles_q, b, tp, tq);
@@ -920,7 +924,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     }
 
-    if (threadIdx.x == kEpiWarp0 * 32) trace_at(p, 7);
+    if (threadIdx.x == kEpiWarp0 * 32) {
+        trace_at(p, 7);
+        if (split) cyc_at(p, 29, cyr);
+    }
     ptx::tc_fence_before();
     if (PAIR) ptx::cluster_sync();   // no CTA of a pair retires while its peer may touch it
     else __syncthreads();

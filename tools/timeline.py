@@ -98,7 +98,8 @@ def main():
           22: "prod: next+decode", 23: "prod: 1st empty wait", 24: "setup: bar init (entry+)",
           25: "setup: L2 prefetch (entry+)", 26: "setup: synced (entry+)",
           27: "setup: dep released (entry+)", 28: "tmem alloc", 29: "epi: 1st tmem ld",
-          30: "epi: chunks issued", 31: "epi: bulk wait read"}
+          30: "epi: chunks issued / split push", 31: "epi: bulk wait read",
+          19: "split: push + own-rows barrier", 29: "split: reduce + C store"}
     for sl, nm in CY.items():
         c = t[1:, :, sl].reshape(-1)
         c = c[c > 0]
