@@ -138,7 +138,7 @@ __device__ __forceinline__ void epi_bar() {   // named barrier over the 8 epilog
     asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
 }
 
-constexpr int kTraceSlots = 32;
+constexpr int kTraceSlots = 40;
 // phase trace (tracing aux subsystem): %globaltimer (ns) at fixed points, 20 slots per CTA
 // (slots 12-15: MMA-issuer cycle counters, see the MMA loop)
 __device__ __forceinline__ void trace_at(const UmmaParams& p, int slot) {
@@ -148,7 +148,7 @@ __device__ __forceinline__ void trace_at(const UmmaParams& p, int slot) {
         p.trace[blockIdx.x * kTraceSlots + slot] = t;
     }
 }
-// cycle-counter stamp (slots 18-31): clock64() - base
+// cycle-counter stamp (slots 18-39): clock64() - base
 __device__ __forceinline__ void cyc_at(const UmmaParams& p, int slot, long long base) {
     if (p.trace) p.trace[blockIdx.x * kTraceSlots + slot] = clock64() - base;
 }
@@ -626,6 +626,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             // stream-K ids: CTAs, or pairs (each CTA of a pair fixes up its own 128 rows)
             const int sk_id = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
             const int sk_G = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+            const bool st1 = threadIdx.x == kEpiWarp0 * 32;     // trace: per-tile stamps
+            const long long cyt0 = st1 && p.trace ? clock64() : 0;
             if (p.streamk && k0 == 0 && nk < p.kb_total && !(p.dbg & 32)) {
                 // owner of a cut tile: the rest of its K range sits in ids sk_id+1 .. c_last.
                 // The contributors published their partials at the START of their ranges,
@@ -635,20 +637,27 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const long long last_unit = (long long)(tile + 1) * p.kb_total - 1;
                 c_last = sk_id;
                 while (c_last + 1 < sk_G && sk_first(c_last + 1, U, sk_G) <= last_unit) ++c_last;
-                // one thread acquires the contributors' flags (backing off between polls so
-                // the publishers' stores are not starved); the named barrier then orders
-                // every epilogue thread's partial reads after that acquire
+                // one thread acquires the contributors' flags (ld.acquire.gpu; a short
+                // back-off after the first misses so the publishers' stores are not
+                // starved); the named barrier then orders every epilogue thread's partial
+                // reads after that acquire
                 if (threadIdx.x == kEpiWarp0 * 32) {
-                    for (int j = c_first; j <= c_last; ++j)
-                        while (atomicAdd(p.flags + sk_slot<PAIR>(j, prank), 0) == 0) __nanosleep(64);
-                    __threadfence();
+                    for (int j = c_first; j <= c_last; ++j) {
+                        int spins = 0;
+                        while (ld_acquire(p.flags + sk_slot<PAIR>(j, prank)) == 0)
+                            if (++spins > 4) __nanosleep(32);
+                    }
                 }
                 epi_bar();
+                if (st1) cyc_at(p, 32, cyt0);
             }
             const int acc = it & 1;
             const uint32_t acc_phase = (it >> 1) & 1;
+            const long long cyt1 = st1 && p.trace ? clock64() : 0;
             ptx::mbar_wait(&tfull[acc], acc_phase);
             ptx::tc_fence_after();
+            if (st1) cyc_at(p, 33, cyt1);
+            const long long cyt2 = st1 && p.trace ? clock64() : 0;
             const bool st0 = it == 0 && threadIdx.x == kEpiWarp0 * 32;
             const long long cye = st0 ? clock64() : 0;
             if (st0) trace_at(p, 5);
@@ -674,11 +683,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) release_acc(&tempty[acc]);
-                __threadfence();
+                // publish: every epilogue thread's partial stores, then the named barrier,
+                // then ONE thread's gpu-scope fence + release store of the flag (cumulative
+                // over the stores the barrier ordered before it)
                 epi_bar();
                 if (threadIdx.x == kEpiWarp0 * 32) {
                     __threadfence();
-                    atomicExch(p.flags + blockIdx.x, 1);
+                    st_release(p.flags + blockIdx.x, 1);
                 }
                 continue;
             }
@@ -766,6 +777,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
                 if (st0) cyc_at(p, 30, cye);
+                if (st1) cyc_at(p, 34, cyt2);
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) release_acc(&tempty[acc]);
@@ -811,7 +823,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (p.dbg & 256) ptx::bulk_wait<0>();
             else ptx::bulk_wait_read<0>();
         }
-        if (threadIdx.x == kEpiWarp0 * 32) cyc_at(p, 31, cyw);
+        if (threadIdx.x == kEpiWarp0 * 32) { cyc_at(p, 31, cyw); cyc_at(p, 35, cyw); }
     }
 
     __syncwarp();  // reconverge the single-lane roles before the .aligned cluster barriers

@@ -19,8 +19,8 @@ import paper_2409_01075_b200 as vx
 import synth
 
 PH = ["entry", "setup", "prod_done", "first_full", "mma_done", "acc_ready", "epi_done",
-      "pre_teardown", "dep_released", "exit", "2nd_issue", "1st_issue", "-", "-", "-", "-", "split_sync1", "split_posted", "-", "-"] + ["-"] * 12
-NS = 32   # slots per CTA; 12-15 = MMA-issuer cycle counters (wait, issue, commit, n), 18-31 cycle stamps
+      "pre_teardown", "dep_released", "exit", "2nd_issue", "1st_issue", "-", "-", "-", "-", "split_sync1", "split_posted", "-", "-"] + ["-"] * 20
+NS = 40   # slots per CTA; 12-15 = MMA-issuer cycle counters (wait, issue, commit, n), 18-31 cycle stamps
 
 
 def main():
@@ -99,7 +99,9 @@ def main():
           25: "setup: L2 prefetch (entry+)", 26: "setup: synced (entry+)",
           27: "setup: dep released (entry+)", 28: "tmem alloc", 29: "epi: 1st tmem ld",
           30: "epi: chunks issued / split push", 31: "epi: bulk wait read",
-          19: "split: push + own-rows barrier", 29: "split: reduce + C store"}
+          19: "split: push + own-rows barrier", 29: "split: reduce + C store",
+          32: "last tile: owner flag acquire", 33: "last tile: accumulator wait",
+          34: "last tile: epilogue chunks", 35: "epi: final bulk wait"}
     for sl, nm in CY.items():
         c = t[1:, :, sl].reshape(-1)
         c = c[c > 0]

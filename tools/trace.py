@@ -8,7 +8,7 @@ import synth
 
 PH = ["entry", "setup", "prod_done", "first_full", "mma_done", "acc_ready", "epi/sync2", "reduced",
       "dep_released", "exit", "first_issue", "-"]
-NS = 32        # slots per CTA (vx_umma.cuh trace_at)
+NS = 40        # slots per CTA (vx_umma.cuh trace_at)
 
 def main():
     a = [x for x in sys.argv[1:] if not x.startswith("--")]
