@@ -97,3 +97,16 @@ def test_device_probe_without_gpu():
     with pytest.raises(vx.VxError) as e:
         vx.device_probe(0)
     assert e.value.status == 5
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    """No CPU or library fallback: the binding refuses to import without libvx.so."""
+    import shutil, subprocess, sys, os
+    pkg = tmp_path / "paper_2409_01075_b200"
+    pkg.mkdir()
+    src = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                       "paper_2409_01075_b200", "__init__.py")
+    shutil.copy(src, pkg / "__init__.py")
+    r = subprocess.run([sys.executable, "-c", "import paper_2409_01075_b200"], cwd=tmp_path,
+                       capture_output=True, text=True)
+    assert r.returncode != 0 and "libvx.so not built" in r.stderr
