@@ -40,7 +40,8 @@ bool kernel_available(int family, int bm, int bn) {
     return false;
 }
 
-using UmmaFn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const UmmaParams);
+using UmmaFn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap,
+                        const CUtensorMap, const UmmaParams);
 
 template <int BN, bool SWAP>
 static UmmaFn pick_mn(bool b_mn) {
@@ -161,6 +162,33 @@ static vx_status make_map(CUtensorMap* map, const void* base, vx_dtype dt, int64
     if (r != CUDA_SUCCESS) {
         set_error("cuTensorMapEncodeTiled failed (%d): inner=%lld rows=%lld batch=%lld ld=%lld",
                   (int)r, (long long)inner, (long long)rows, (long long)batch, (long long)ld);
+        return VX_ERR_CUDA;
+    }
+    return VX_OK;
+}
+
+// 4-D two-chunk view of a K-major 16-bit matrix [batch][rows][K] (K % 64 == 0): dims
+// {64 k, rows, K/64 chunks, batch}, strides {ld, 128 B, batch}; box {64, box_rows, 2, 1}.
+// One box = two consecutive 64-deep chunks of box_rows rows, written chunk-major: the second
+// lands box_rows * 128 B after the first, i.e. exactly in the next ring stage's slot, with
+// the same 128-B swizzle (the pattern is a function of the SMEM address).
+static vx_status make_map_k2(CUtensorMap* map, const void* base, vx_dtype dt, int64_t K,
+                             int64_t rows, int64_t batch, int64_t ld, int64_t bstride,
+                             int box_rows) {
+    EncodeTiledFn enc = encode_fn();
+    if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return VX_ERR_CUDA; }
+    cuuint64_t dims[4] = {64, (cuuint64_t)rows, (cuuint64_t)(K / 64), (cuuint64_t)batch};
+    cuuint64_t strides[3] = {(cuuint64_t)ld * 2, 128, (cuuint64_t)bstride * 2};
+    cuuint32_t box[4] = {64, (cuuint32_t)box_rows, 2, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    const CUtensorMapDataType ty = dt == VX_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                                 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+    CUresult r = enc(map, ty, 4, const_cast<void*>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        set_error("two-chunk cuTensorMapEncodeTiled failed (%d): K=%lld rows=%lld", (int)r,
+                  (long long)K, (long long)rows);
         return VX_ERR_CUDA;
     }
     return VX_OK;
@@ -334,6 +362,22 @@ vx_status launch(const vx_plan_s* p, const vx_choice& ch, int64_t batch, int64_t
                 ((uint32_t)(r.bn >> 3) << 17) | ((uint32_t)((pair ? 256 : 128) >> 4) << 24);
     prm.pair = pair ? 1 : 0;
     prm.bpack = p->bl == VX_B_PACKED ? 1 : 0;
+    // deep-K units: K-major P and Q, whole 64-deep chunks, non-pair,
+    // unpacked, and a ring of >= 6 stages (with 4 stages = 2 units in flight the MMA waits
+    // on whole 128-deep units: 128 x 256 rungs measured up to 1.17x slower);
+    // VX_DEBUG_FLAGS bit 4096 turns them off (A/B timing only)
+    prm.kdouble = (!pair && !b_mn && p->bl != VX_B_PACKED && K % 64 == 0 && K >= 128 &&
+                   r.stages >= 6 && !(g_dbg & 4096)) ? 1 : 0;
+    CUtensorMap mapA2, mapB2;
+    if (prm.kdouble) {
+        s = make_map_k2(&mapA2, A, p->in, K, M, batch, K, batch > 1 ? sA : M * K, a_box);
+        if (s != VX_OK) return s;
+        s = make_map_k2(&mapB2, B, p->in, K, N, batch, K, batch > 1 ? sB : N * K, swap ? 128 : r.bn);
+        if (s != VX_OK) return s;
+    } else {
+        mapA2 = mapA;
+        mapB2 = mapB;
+    }
     prm.C = C;
     prm.ldc = N;
     prm.sC = batch > 1 ? sC : M * N;
@@ -378,7 +422,9 @@ vx_status launch(const vx_plan_s* p, const vx_choice& ch, int64_t batch, int64_t
     // P operand (UMMA-M axis) first: A for family 0, B for the swapped family
     const CUtensorMap& mapP = swap ? mapB : mapA;
     const CUtensorMap& mapQ = swap ? mapA : mapB;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, fn, mapP, mapQ, mapC, prm);
+    const CUtensorMap& mapP2 = swap ? mapB2 : mapA2;
+    const CUtensorMap& mapQ2 = swap ? mapA2 : mapB2;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, fn, mapP, mapQ, mapC, mapP2, mapQ2, prm);
     if (e != cudaSuccess) return cuda_fail(e, "tcgen05 launch");
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return VX_OK;

@@ -66,6 +66,9 @@ struct UmmaParams {
     int bpack;                  // 1: B is VX_B_PACKED (5-D map of 64 x 64 contiguous tiles)
     float* ws;                  // stream-K partial slots [gridDim.x][128][BN] fp32 (plan-owned)
     int* flags;                 // stream-K slot-ready flags [gridDim.x] (0 between launches)
+    int kdouble;                // 1: two-chunk loads (tmP2 / tmQ2) fill two adjacent ring
+                                // stages with one TMA box per operand (K % 64 == 0, K-major
+                                // P and Q, non-pair, unpacked; DESIGN.md 4.1 "deep-K units")
 };
 
 // ---- work assignment (the L3 schedule of the rung) ---------------------------------------
@@ -333,7 +336,8 @@ __device__ __forceinline__ void sk_reset(const UmmaParams& p, int c0, int c1, ui
 template <int BN, bool SWAP, bool P_MN, bool Q_MN, bool PAIR = false>
 __global__ void __launch_bounds__(kThreads, 1)
     vx_umma_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmQ,
-                   const __grid_constant__ CUtensorMap tmC, const __grid_constant__ UmmaParams p) {
+                   const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmP2,
+                   const __grid_constant__ CUtensorMap tmQ2, const __grid_constant__ UmmaParams p) {
     static_assert(!PAIR || !SWAP, "pair rungs are non-swapped");
     using Cfg = UmmaCfg<BN>;
     constexpr int kP = Cfg::kPBytes;
@@ -363,6 +367,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::prefetch_tmap(&tmP);
         ptx::prefetch_tmap(&tmQ);
         if (p.vec) ptx::prefetch_tmap(&tmC);
+        if (p.kdouble) {
+            ptx::prefetch_tmap(&tmP2);
+            ptx::prefetch_tmap(&tmQ2);
+        }
         for (int i = 0; i < S; ++i) {
             ptx::mbar_init(&full[i], 1);
             ptx::mbar_init(&empty[i], 1);
@@ -403,6 +411,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             // ===== TMA producers: producer `pid` takes this CTA's k-blocks j % 2 == pid =====
             const int pid = warp == 0 ? 0 : 1;
+            const bool kd = p.kdouble && !PAIR && !P_MN && !Q_MN && !p.bpack;
             const long long cy0 = p.trace ? clock64() : 0;   // trace: setup -> first issue
             const uint64_t pol = (p.dbg & 1024) ? ptx::policy_evict_first()
                                : (p.dbg & 2048) ? ptx::policy_evict_normal()
@@ -441,11 +450,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                 decode_tile(tile, p.tiles_p, p.tiles_q, b, tp, tq);
                 if (pid == 0 && j == 0) cyc_at(p, 22, cy0);
                 for (int kb = k0; kb < k0 + nk; ++kb, ++j) {
+                    // a unit is one k-block, or two (deep-K) when the next k-block of this
+                    // range lands in the next ring stage without a wrap; the MMA issuer walks
+                    // the same rule; j counts units, alternating between the producers
+                    const bool dbl = kd && kb + 1 < k0 + nk && stage + 1 < S;
                     if (j % kProdWarps != pid) {
+                        if (dbl) { ++kb; ++stage; }
                         if (++stage == S) { stage = 0; phase ^= 1; }
                         continue;
                     }
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
+                    if (dbl) ptx::mbar_wait(&empty[stage + 1], phase ^ 1);
                     if (j == 0) cyc_at(p, 23, cy0);
                     if (kb >= k0 + kProdWarps && !stamped) { trace_at(p, 10); stamped = true; }
                     uint8_t* dP = sP + stage * kP;
@@ -477,6 +492,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     if (!stamped && kb == k0 && p.trace) {
                         p.trace[blockIdx.x * kTraceSlots + 18] = clock64() - cy0;
+                    }
+                    if (dbl) {
+                        // both chunks complete on full[stage]; full[stage + 1] gets a plain
+                        // arrive so every barrier still completes once per ring round
+                        ptx::mbar_arrive_expect_tx(&full[stage], 2 * (kP + kQ));
+                        ptx::mbar_arrive(&full[stage + 1]);
+                        dep_wait(tile, kb, k0 + nk - kb);
+                        if (!stamped && kb == k0) trace_at(p, 11);
+                        ptx::tma_load_4d(dP, &tmP2, &full[stage], 0, tp * 128, kb, b, pol);
+                        ptx::tma_load_4d(dQ, &tmQ2, &full[stage], 0, tq * BN, kb, b, pol);
+                        ++kb;
+                        stage += 2;
+                        if (stage == S) { stage = 0; phase ^= 1; }
+                        continue;
                     }
                     ptx::mbar_arrive_expect_tx(&full[stage], kP + kQ);
                     dep_wait(tile, kb, k0 + nk - kb);
@@ -540,6 +569,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             int stage = 0;
             uint32_t phase = 0;
             int it = 0;
+            const bool kd = p.kdouble && !PAIR && !P_MN && !Q_MN && !p.bpack;
             WorkIter wi(p, rank);
             int tile, k0, nk;
             for (; wi.next(p, tile, k0, nk); ++it) {
@@ -548,10 +578,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
                 ptx::tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
+                bool second = false;   // this k-block landed with the previous one (deep-K unit)
                 for (int i = 0; i < nk; ++i) {
                     const long long c0 = tr ? clock64() : 0;
-                    ptx::mbar_wait(&full[stage], phase);
-                    ptx::tc_fence_after();
+                    if (second) {
+                        second = false;
+                    } else {
+                        ptx::mbar_wait(&full[stage], phase);
+                        ptx::tc_fence_after();
+                        second = kd && i + 1 < nk && stage + 1 < S;   // producers' rule
+                    }
                     const long long c1 = tr ? clock64() : 0;
                     if (it == 0 && i == 0 && lane == 0) trace_at(p, 3);
                     const uint64_t dp0 = dP_base + (uint64_t)(stage * (kP >> 4));

@@ -69,6 +69,25 @@ def test_every_rung_and_split_integer_exact(bl, out):
                 assert np.array_equal(got, want), (M, r, s, np.abs(got - want).max())
 
 
+@pytest.mark.gpu
+def test_deep_k_units_odd_kblock_counts():
+    # K = 704: 11 k-blocks, so every persistent tile ends on a single k-block after the
+    # two-chunk (deep-K) units, the ring wraps mid-pair-sequence, and stream-K ranges start
+    # and end at odd offsets (DESIGN.md 4.1 deep-K units); integer data -> bit-exact
+    vx = vxmod()
+    N, K = 256, 704
+    p = vx.Plan(N, K, "bf16", "fp32", "nk")
+    for M in (1, 129, 300):
+        A, B = synth.gemm_inputs(M, N, K, "bf16", "nk", kind="int", seed=7 + M)
+        want = _round_to(oracle.gemm(A, B, "nk"), "fp32")
+        for r in p.dump()["rungs"]:
+            if not _ok(r, M):
+                continue
+            for s in r["splits"]:
+                got, _ = _run(p, A, B, force=(r["rung_id"], s))
+                assert np.array_equal(got, want), (M, r["rung_id"], s)
+
+
 def test_fp16_inputs_integer_exact():
     vx = vxmod()
     N, K = 256, 320                       # K not a multiple of 64: TMA zero-fills the K tail
