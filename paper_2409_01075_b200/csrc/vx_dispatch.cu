@@ -362,17 +362,18 @@ vx_status launch(const vx_plan_s* p, const vx_choice& ch, int64_t batch, int64_t
                 ((uint32_t)(r.bn >> 3) << 17) | ((uint32_t)((pair ? 256 : 128) >> 4) << 24);
     prm.pair = pair ? 1 : 0;
     prm.bpack = p->bl == VX_B_PACKED ? 1 : 0;
-    // deep-K units: K-major P and Q, whole 64-deep chunks, non-pair,
-    // unpacked, and a ring of >= 6 stages (with 4 stages = 2 units in flight the MMA waits
-    // on whole 128-deep units: 128 x 256 rungs measured up to 1.17x slower);
-    // VX_DEBUG_FLAGS bit 4096 turns them off (A/B timing only)
-    prm.kdouble = (!pair && !b_mn && p->bl != VX_B_PACKED && K % 64 == 0 && K >= 128 &&
-                   r.stages >= 6 && !(g_dbg & 4096)) ? 1 : 0;
+    // deep-K units: K-major P and Q, whole 64-deep chunks, unpacked, and a
+    // ring deep enough to keep >= 3 units (>= 4 for the compute-bound pair rungs) in flight:
+    // measured, 128 x 256 (4 stages) up to 1.17x slower, pair 256 x 256 (6 stages) 1.03x
+    // slower, pair 256 x 128 (8 stages) 0.86-0.90x; VX_DEBUG_FLAGS bit 4096 turns them off
+    // (A/B timing only)
+    prm.kdouble = (!b_mn && p->bl != VX_B_PACKED && K % 64 == 0 && K >= 128 &&
+                   r.stages >= (pair ? 8 : 6) && !(g_dbg & 4096)) ? 1 : 0;
     CUtensorMap mapA2, mapB2;
     if (prm.kdouble) {
         s = make_map_k2(&mapA2, A, p->in, K, M, batch, K, batch > 1 ? sA : M * K, a_box);
         if (s != VX_OK) return s;
-        s = make_map_k2(&mapB2, B, p->in, K, N, batch, K, batch > 1 ? sB : N * K, swap ? 128 : r.bn);
+        s = make_map_k2(&mapB2, B, p->in, K, N, batch, K, batch > 1 ? sB : N * K, swap ? 128 : (pair ? r.bn / 2 : r.bn));
         if (s != VX_OK) return s;
     } else {
         mapA2 = mapA;

@@ -138,6 +138,15 @@ __device__ __forceinline__ void tma_load_5d_pair(void* dst, const void* tmap, ui
 // cta_group::2 tile load: bytes land in THIS CTA's shared memory, completion is counted
 // on the pair leader's mbarrier (same offset, peer bit cleared -- CUTLASS's
 // Sm100MmaPeerBitMask convention)
+__device__ __forceinline__ void tma_load_4d_pair(void* dst, const void* tmap, uint64_t* bar, int c0,
+                                                 int c1, int c2, int c3, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3, %4, %5}], [%6], %7;" ::"r"(smem_addr(dst)),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+        "r"(smem_addr(bar) & 0xFEFFFFFFu), "l"(policy)
+        : "memory");
+}
 __device__ __forceinline__ void tma_load_3d_pair(void* dst, const void* tmap, uint64_t* bar, int c0,
                                                  int c1, int c2, uint64_t policy) {
     asm volatile(

@@ -411,7 +411,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             // ===== TMA producers: producer `pid` takes this CTA's k-blocks j % 2 == pid =====
             const int pid = warp == 0 ? 0 : 1;
-            const bool kd = p.kdouble && !PAIR && !P_MN && !Q_MN && !p.bpack;
+            const bool kd = p.kdouble && !P_MN && !Q_MN && !p.bpack;
             const long long cy0 = p.trace ? clock64() : 0;   // trace: setup -> first issue
             const uint64_t pol = (p.dbg & 1024) ? ptx::policy_evict_first()
                                : (p.dbg & 2048) ? ptx::policy_evict_normal()
@@ -465,6 +465,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (kb >= k0 + kProdWarps && !stamped) { trace_at(p, 10); stamped = true; }
                     uint8_t* dP = sP + stage * kP;
                     uint8_t* dQ = sQ + stage * kQ;
+                    if (PAIR && dbl) {
+                        // deep-K unit of a pair: both CTAs' two-chunk boxes complete on the
+                        // leader's full[stage]; the leader's full[stage + 1] gets a plain arrive
+                        if (prank == 0) {
+                            ptx::mbar_arrive_expect_tx(&full[stage], 4 * (kP + kQ));
+                            ptx::mbar_arrive(&full[stage + 1]);
+                        }
+                        dep_wait(tile, kb, k0 + nk - kb);
+                        ptx::tma_load_4d_pair(dP, &tmP2, &full[stage], 0, tp * 256 + (int)prank * 128,
+                                              kb, b, pol);
+                        ptx::tma_load_4d_pair(dQ, &tmQ2, &full[stage], 0,
+                                              tq * BN + (int)prank * (BN / 2), kb, b, pol);
+                        ++kb;
+                        stage += 2;
+                        if (stage == S) { stage = 0; phase ^= 1; }
+                        continue;
+                    }
                     if (PAIR) {
                         // both halves complete on the leader's full barrier
                         if (prank == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2 * (kP + kQ));
@@ -569,7 +586,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             int stage = 0;
             uint32_t phase = 0;
             int it = 0;
-            const bool kd = p.kdouble && !PAIR && !P_MN && !Q_MN && !p.bpack;
+            const bool kd = p.kdouble && !P_MN && !Q_MN && !p.bpack;
             WorkIter wi(p, rank);
             int tile, k0, nk;
             for (; wi.next(p, tile, k0, nk); ++it) {
