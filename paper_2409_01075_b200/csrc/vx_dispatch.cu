@@ -290,7 +290,24 @@ vx_status launch(const vx_plan_s* p, const vx_choice& ch, int64_t batch, int64_t
         case 8: fn = kn ? vx_gemv_kernel<8, true> : vx_gemv_kernel<8, false>; break;
         }
         if (!fn || M > r.bm) { set_error("no GEMV kernel for rung %d / M=%lld", r.rung_id, (long long)M); return VX_ERR_UNSUPPORTED; }
+        // MT >= 4, N x K B: A staged once in shared memory (R20b); VX_DEBUG_FLAGS 16384 = off
+        size_t a_smem = 0;
+        if (!kn && r.bm >= 4 && K % 8 == 0 && !(g_dbg & 16384) &&
+            (size_t)r.bm * K * 2 <= kGemvSaMaxSmem) {
+            fn = r.bm == 4 ? vx_gemv_sa_kernel<4, 4> : vx_gemv_sa_kernel<8, 2>;
+            a_smem = (size_t)r.bm * K * 2;
+            static bool attr_set[2] = {false, false};
+            bool& done = attr_set[r.bm == 8];
+            if (!done) {
+                cudaError_t ea = cudaFuncSetAttribute((const void*)fn,
+                                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                      (int)kGemvSaMaxSmem);
+                if (ea != cudaSuccess) return cuda_fail(ea, "GEMV smem attribute");
+                done = true;
+            }
+        }
         cudaLaunchConfig_t cfg = {};
+        cfg.dynamicSmemBytes = a_smem;
         cfg.gridDim = dim3((unsigned)cdiv(N, kGemvCols), (unsigned)batch, 1);
         cfg.blockDim = dim3(kGemvWarps * 32, 1, 1);
         cfg.stream = st;

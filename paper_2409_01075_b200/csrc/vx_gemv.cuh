@@ -20,6 +20,7 @@ constexpr int kGemvWarps = 8;
 constexpr int kGemvNC = 4;                        // columns per warp
 constexpr int kGemvKS = 4;                        // K slices per CTA (warps sharing columns)
 constexpr int kGemvCols = kGemvWarps / kGemvKS * kGemvNC;   // columns per CTA (8)
+constexpr size_t kGemvSaMaxSmem = 96 * 1024;   // A-in-SMEM variant: MT * K * 2 bytes max
 
 __device__ __forceinline__ void unpack8(uint4 u, float* f, int kind) {
     const uint32_t w[4] = {u.x, u.y, u.z, u.w};
@@ -112,6 +113,101 @@ __global__ void __launch_bounds__(kGemvWarps * 32)
         }
     }
     // warp reduction (fixed butterfly order -> deterministic), then across the K slices
+#pragma unroll
+    for (int m = 0; m < MT; ++m)
+#pragma unroll
+        for (int c = 0; c < kGemvNC; ++c)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc[m][c] += __shfl_xor_sync(0xffffffffu, acc[m][c], o);
+    if (lane == 0) {
+#pragma unroll
+        for (int m = 0; m < MT; ++m)
+#pragma unroll
+            for (int c = 0; c < kGemvNC; ++c) red[ks][cg][m][c] = acc[m][c];
+    }
+    __syncthreads();
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    for (int i = threadIdx.x; i < CG * MT * kGemvNC; i += blockDim.x) {
+        const int g = i / (MT * kGemvNC), m = i / kGemvNC % MT, c = i % kGemvNC;
+        const int n = blockIdx.x * kGemvCols + g * kGemvNC + c;
+        if (m >= M || n >= N) continue;
+        float v = red[0][g][m][c];
+#pragma unroll
+        for (int j = 1; j < kGemvKS; ++j) v += red[j][g][m][c];
+        const long long idx = b * sC + (long long)m * N + n;
+        if (out_kind == 2) reinterpret_cast<float*>(C)[idx] = v;
+        else if (out_kind == 0) reinterpret_cast<__nv_bfloat16*>(C)[idx] = __float2bfloat16_rn(v);
+        else reinterpret_cast<__half*>(C)[idx] = __float2half_rn(v);
+    }
+}
+
+// Variant for MT >= 4 with B stored N x K (R20b): the per-iteration A loads of the kernel
+// above (MT more 16-B loads per step, each an L2 round trip on the critical path, and MT x 4
+// more live registers) are what starve it of B bytes in flight at MT = 4 / 8.  Here each CTA
+// first issues the B loads of its first U k-steps, then stages A (MT x K bf16/fp16, rows >= M
+// zero) into shared memory once, and the k-steps read A from shared memory; the registers
+// saved hold U steps of B instead.  Same column / K-slice ownership and reduction order as
+// vx_gemv_kernel.  Requires K % 8 == 0 and MT * K * 2 <= the dynamic smem the dispatcher sets.
+template <int MT, int U>
+__global__ void __launch_bounds__(kGemvWarps * 32)
+    vx_gemv_sa_kernel(const uint16_t* __restrict__ A, const uint16_t* __restrict__ B, void* C,
+                      int M, int N, int K, long long sA, long long sB, long long sC, int in_kind,
+                      int out_kind) {
+    constexpr int CG = kGemvWarps / kGemvKS;
+    extern __shared__ __align__(16) uint16_t a_sm[];          // [MT][K]
+    __shared__ float red[kGemvKS][CG][MT][kGemvNC];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int cg = warp % CG, ks = warp / CG;
+    const int b = blockIdx.y;
+    const int n0 = blockIdx.x * kGemvCols + cg * kGemvNC;
+    A += b * sA;
+    B += b * sB;
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    constexpr int KSTEP = kGemvKS * 256;
+    int k = (ks * 32 + lane) * 8;
+    uint4 braw[U][kGemvNC];
+    auto load_b = [&](int kb) {
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int c = 0; c < kGemvNC; ++c)
+                braw[u][c] = (kb + u * KSTEP < K && n0 + c < N)
+                                 ? ldg16(B + (long long)(n0 + c) * K + kb + u * KSTEP)
+                                 : make_uint4(0, 0, 0, 0);
+    };
+    load_b(k);
+    const int k8 = K >> 3;
+    for (int i = threadIdx.x; i < MT * k8; i += blockDim.x) {
+        const int m = i / k8, kk = (i - m * k8) * 8;
+        reinterpret_cast<uint4*>(a_sm)[i] =
+            m < M ? ldg16(A + (long long)m * K + kk) : make_uint4(0, 0, 0, 0);
+    }
+    __syncthreads();
+    float acc[MT][kGemvNC];
+#pragma unroll
+    for (int m = 0; m < MT; ++m)
+#pragma unroll
+        for (int c = 0; c < kGemvNC; ++c) acc[m][c] = 0.f;
+    for (; k < K; k += U * KSTEP) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int kk = k + u * KSTEP;
+            if (kk >= K) break;
+            float bv[kGemvNC][8];
+#pragma unroll
+            for (int c = 0; c < kGemvNC; ++c) unpack8(braw[u][c], bv[c], in_kind);
+#pragma unroll
+            for (int m = 0; m < MT; ++m) {
+                float av[8];
+                unpack8(*reinterpret_cast<const uint4*>(a_sm + m * K + kk), av, in_kind);
+#pragma unroll
+                for (int c = 0; c < kGemvNC; ++c)
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) acc[m][c] = fmaf(av[e], bv[c][e], acc[m][c]);
+            }
+        }
+        if (k + U * KSTEP < K) load_b(k + U * KSTEP);
+    }
 #pragma unroll
     for (int m = 0; m < MT; ++m)
 #pragma unroll

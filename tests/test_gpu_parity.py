@@ -403,3 +403,23 @@ def test_gemv_column_tail_nk():
             if M <= r["bm"]:
                 got, _ = _run(p, A, B, force=(r["rung_id"], 1))
                 assert np.array_equal(got, want), (M, r["bm"])
+
+
+@pytest.mark.gpu
+def test_gemv_a_in_smem_long_k():
+    """R20b: the MT 4 / 8 GEMV rungs with N x K B stage A in shared memory and keep U k-steps
+    of B in flight per warp.  K = 5000 gives 5 k-steps per warp slice (several U chunks and a
+    ragged last step); K = 7000 puts MT = 8 over the SMEM cap (falls back to the plain
+    kernel) while MT = 4 still stages A.  Integer-exact, N tail, M below and at MT."""
+    vx = vxmod()
+    N = 204
+    for K in (5000, 7000):
+        p = vx.Plan(N, K, "bf16", "fp32", "nk")
+        rungs = [r for r in p.dump()["rungs"] if r["family"] == 3 and r["bm"] >= 4]
+        for M in (3, 4, 6, 8):
+            A, B = synth.gemm_inputs(M, N, K, "bf16", "nk", kind="int", seed=90 + M)
+            want = oracle.gemm(A, B, "nk")
+            for r in rungs:
+                if M <= r["bm"]:
+                    got, _ = _run(p, A, B, force=(r["rung_id"], 1))
+                    assert np.array_equal(got, want), (K, M, r["bm"])
