@@ -290,9 +290,11 @@ vx_status launch(const vx_plan_s* p, const vx_choice& ch, int64_t batch, int64_t
         case 8: fn = kn ? vx_gemv_kernel<8, true> : vx_gemv_kernel<8, false>; break;
         }
         if (!fn || M > r.bm) { set_error("no GEMV kernel for rung %d / M=%lld", r.rung_id, (long long)M); return VX_ERR_UNSUPPORTED; }
-        // MT >= 4, N x K B: A staged once in shared memory (R20b); VX_DEBUG_FLAGS 16384 = off
+        // MT >= 4, N x K B, K >= 2048 (>= 2 k-steps per warp; below that the staging is
+        // pure latency: BERT K = 768, M = 4 measured 3.5 -> 4.4 us): A staged once in shared
+        // memory (R20b); VX_DEBUG_FLAGS 16384 = off
         size_t a_smem = 0;
-        if (!kn && r.bm >= 4 && K % 8 == 0 && !(g_dbg & 16384) &&
+        if (!kn && r.bm >= 4 && K % 8 == 0 && K >= 2048 && !(g_dbg & 16384) &&
             (size_t)r.bm * K * 2 <= kGemvSaMaxSmem) {
             fn = r.bm == 4 ? vx_gemv_sa_kernel<4, 4> : vx_gemv_sa_kernel<8, 2>;
             a_smem = (size_t)r.bm * K * 2;
