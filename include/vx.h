@@ -19,21 +19,33 @@
  *
  * Conventions for every entry point
  *   - Memory: A, B, C are DEVICE pointers owned by the caller (e.g. torch tensors); the
- *     library never allocates device memory on the hot path and never copies to the host.
+ *     library never copies to the host and allocates device memory only for the stream-K
+ *     workspace of a stream, once, on that stream's first stream-K launch (see Thread
+ *     safety); vx_plan pre-allocates the legacy stream's.
  *   - Layout: row-major with a contiguous inner dimension.  A is [M,K] (K contiguous).
  *     B is [K,N] (VX_B_KN, the paper's B) or [N,K] (VX_B_NK, an nn.Linear weight / K^T of
  *     attention).  C is [M,N] (N contiguous).  Batched: element (b,i,j) of X lives at
  *     X + b*sX + (row-major offset), strides sX in ELEMENTS.
- *   - Alignment (TMA): 16-bit inputs need K % 8 == 0, N % 8 == 0, 16-byte aligned base
- *     pointers and batch strides that are multiples of 8 elements; otherwise VX_ERR_ALIGN.
- *     There is no silent fallback and no CPU fallback.
+ *   - Alignment (TMA): 16-bit inputs need K % 8 == 0, 16-byte aligned A and B base
+ *     pointers and A/B batch strides that are multiples of 8 elements; B stored K x N
+ *     (VX_B_KN) additionally needs N % 8 == 0 (its row stride is N elements).  C needs only
+ *     element alignment (rows that are not 16-B aligned are written with scalar stores).
+ *     Violations return VX_ERR_ALIGN.  There is no silent fallback and no CPU fallback.
  *   - Streams are passed as `void*` holding a cudaStream_t (NULL = legacy default stream).
  *   - Asynchrony: vx_gemm* enqueue work and return; device faults surface at the caller's
  *     next synchronisation.  Launch errors are returned as VX_ERR_CUDA.
  *   - Errors: every function returns a vx_status; vx_last_error() gives a thread-local
  *     one-line detail for the most recent failure on the calling thread.
- *   - Thread safety: a plan is immutable after creation; concurrent vx_gemm calls with the
- *     same plan on different streams are safe.
+ *   - Thread safety: a plan's strategy table is immutable after creation (selections are
+ *     memoised in a write-once table) and concurrent vx_gemm calls with the same plan on
+ *     different streams are safe: the only mutable device state, the stream-K partial
+ *     workspace, is kept per (device, stream) -- allocated on the first stream-K launch on
+ *     a stream (inside a capture that allocation runs in relaxed capture mode), reused by
+ *     later launches on that stream, which the stream serialises.  Two CUDA graphs
+ *     captured on the same stream share that stream's workspace, so they must not be
+ *     replayed concurrently.
+ *   - Device: a plan from vx_plan(device=d) launches only while d is the calling thread's
+ *     current device (VX_ERR_INVALID otherwise).
  */
 #ifndef VX_H
 #define VX_H

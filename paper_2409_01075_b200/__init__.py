@@ -226,12 +226,23 @@ class Plan:
                 raise ValueError("%s must be a contiguous CUDA tensor" % nm)
             if _dt_name(t) != self.in_dtype:
                 raise ValueError("%s dtype %s != plan input %s" % (nm, t.dtype, self.in_dtype))
+        if B.device != A.device:
+            raise ValueError("A and B must be on the same device")
+        if A.dim() == 3 and self.b_layout != "packed":
+            # batched: B must carry the same batch dimension (the C call reads batch*N*K
+            # elements of B at stride N*K; a 2-D B would be read past its end)
+            if B.dim() != 3 or B.shape[0] != batch:
+                raise ValueError("batched A [%d,M,K] needs B of shape [%d,...]" % (batch, batch))
+        elif A.dim() == 2 and B.dim() != 2 and self.b_layout != "packed":
+            raise ValueError("2-D A needs a 2-D B")
         odt = {"bf16": torch.bfloat16, "fp16": torch.float16, "fp32": torch.float32}[self.out_dtype]
         shape = (M, N) if A.dim() == 2 else (batch, M, N)
         if out is None:
             out = torch.empty(shape, dtype=odt, device=A.device)
         elif out.dtype != odt or tuple(out.shape) != shape or not out.is_contiguous():
             raise ValueError("out must be a contiguous %s tensor of shape %s" % (odt, shape))
+        elif out.device != A.device:
+            raise ValueError("out must be on A's device")
         ch = Choice()
         fr, fs = force if force is not None else (-1, 0)
         _check(_lib.vx_gemm_ex(self._h, batch, M, N, K, A.data_ptr(), M * K, B.data_ptr(), N * K,

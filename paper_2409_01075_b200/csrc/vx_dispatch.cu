@@ -104,22 +104,37 @@ static vx_status cuda_fail(cudaError_t e, const char* what) {
     return VX_ERR_CUDA;
 }
 
-// one-time per-kernel attribute setup (max dynamic smem; cluster dims are per launch)
+// one-time per-(device, kernel) attribute setup (max dynamic smem; cluster dims are per
+// launch).  cudaFuncSetAttribute applies to the CURRENT device only, so the cache is keyed
+// by (device, function).
 static std::mutex g_attr_mu;
 static vx_status ensure_attr(const void* fn, int64_t smem) {
-    static const void* done[64];
-    static int64_t done_smem[64];
+    struct Entry { int dev; const void* fn; int64_t smem; };
+    static Entry done[256];
     static int ndone = 0;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
     std::lock_guard<std::mutex> lk(g_attr_mu);
     for (int i = 0; i < ndone; ++i)
-        if (done[i] == fn && done_smem[i] >= smem) return VX_OK;
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (done[i].dev == dev && done[i].fn == fn && done[i].smem >= smem) return VX_OK;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
     for (int i = 0; i < ndone; ++i)
-        if (done[i] == fn) { done_smem[i] = smem; return VX_OK; }
-    if (ndone < 64) { done[ndone] = fn; done_smem[ndone] = smem; ++ndone; }
+        if (done[i].dev == dev && done[i].fn == fn) { done[i].smem = smem; return VX_OK; }
+    if (ndone < 256) done[ndone++] = {dev, fn, smem};
     return VX_OK;
 }
+
+// restores the calling thread's current device on scope exit
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        if (dev >= 0 && cudaGetDevice(&prev) == cudaSuccess && prev != dev) cudaSetDevice(dev);
+        else prev = -1;
+    }
+    ~DeviceGuard() { if (prev >= 0) cudaSetDevice(prev); }
+};
 
 // ---- CUtensorMap encoding via the driver entry point (no -lcuda link dependency) -------
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -239,24 +254,42 @@ __global__ void vx_pack_b_kernel(const uint16_t* __restrict__ B, uint16_t* __res
 
 static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
-// stream-K workspace: one partial slot (128 x 256 fp32) + one flag per SM, allocated once
-// per plan on its device (outside any graph capture: vx_plan allocates it eagerly)
+// stream-K workspace: one partial slot (128 x 256 fp32) + one flag per SM.  One workspace
+// per (device, stream): stream-K launches on one stream are serialised by the stream, and
+// every flag is consumed and cleared inside the launch that set it, so a stream's
+// workspace is always clean for its next launch; launches on different streams use
+// different workspaces (vx.h thread-safety contract).  Allocated on first stream-K use of
+// a stream (vx_plan pre-allocates one for the legacy stream).  If that first use happens
+// inside a stream capture, the allocation runs in relaxed capture mode and the flags are
+// zeroed on a private non-blocking stream that is synchronised before returning, so
+// neither touches the captured stream.
 static size_t ws_bytes(const vx_plan_s* p) {
     return (size_t)p->desc.sm_count * 128 * 256 * 4 + (size_t)p->desc.sm_count * 4 + 256;
 }
-static vx_status ensure_ws(const vx_plan_s* pc) {
+static vx_status ensure_ws(const vx_plan_s* pc, void* stream, void** out) {
     vx_plan_s* p = const_cast<vx_plan_s*>(pc);
-    std::lock_guard<std::mutex> lk(p->ws_mu);
-    if (p->ws) return VX_OK;
     int dev = 0;
-    cudaGetDevice(&dev);
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    std::lock_guard<std::mutex> lk(p->ws_mu);
+    for (const auto& w : p->ws)
+        if (w.stream == stream && w.device == dev) { *out = w.ptr; return VX_OK; }
+    cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+    cudaThreadExchangeStreamCaptureMode(&mode);
     void* w = nullptr;
-    cudaError_t e = cudaMalloc(&w, ws_bytes(p));
-    if (e != cudaSuccess) return cuda_fail(e, "stream-K workspace cudaMalloc");
-    e = cudaMemset(w, 0, ws_bytes(p));
-    if (e != cudaSuccess) { cudaFree(w); return cuda_fail(e, "stream-K workspace memset"); }
-    p->ws = w;
-    p->ws_device = dev;
+    cudaStream_t priv = nullptr;
+    e = cudaMalloc(&w, ws_bytes(p));
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&priv, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaMemsetAsync(w, 0, ws_bytes(p), priv);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(priv);
+    if (priv) cudaStreamDestroy(priv);
+    cudaThreadExchangeStreamCaptureMode(&mode);
+    if (e != cudaSuccess) {
+        if (w) cudaFree(w);
+        return cuda_fail(e, "stream-K workspace allocation");
+    }
+    p->ws.push_back({stream, dev, w});
+    *out = w;
     return VX_OK;
 }
 
@@ -298,15 +331,8 @@ vx_status launch(const vx_plan_s* p, const vx_choice& ch, int64_t batch, int64_t
             (size_t)r.bm * K * 2 <= kGemvSaMaxSmem) {
             fn = r.bm == 4 ? vx_gemv_sa_kernel<4, 4> : vx_gemv_sa_kernel<8, 2>;
             a_smem = (size_t)r.bm * K * 2;
-            static bool attr_set[2] = {false, false};
-            bool& done = attr_set[r.bm == 8];
-            if (!done) {
-                cudaError_t ea = cudaFuncSetAttribute((const void*)fn,
-                                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                      (int)kGemvSaMaxSmem);
-                if (ea != cudaSuccess) return cuda_fail(ea, "GEMV smem attribute");
-                done = true;
-            }
+            vx_status sa = ensure_attr((const void*)fn, (int64_t)kGemvSaMaxSmem);
+            if (sa != VX_OK) return sa;
         }
         cudaLaunchConfig_t cfg = {};
         cfg.dynamicSmemBytes = a_smem;
@@ -366,10 +392,11 @@ vx_status launch(const vx_plan_s* p, const vx_choice& ch, int64_t batch, int64_t
     prm.ws = nullptr;
     prm.flags = nullptr;
     if (prm.streamk) {
-        s = ensure_ws(p);
+        void* w = nullptr;
+        s = ensure_ws(p, stream, &w);
         if (s != VX_OK) return s;
-        prm.ws = reinterpret_cast<float*>(p->ws);
-        prm.flags = reinterpret_cast<int*>(reinterpret_cast<char*>(p->ws) +
+        prm.ws = reinterpret_cast<float*>(w);
+        prm.flags = reinterpret_cast<int*>(reinterpret_cast<char*>(w) +
                                            (size_t)p->desc.sm_count * 128 * 256 * 4);
     }
     prm.stages = r.stages;
@@ -451,8 +478,10 @@ vx_status launch(const vx_plan_s* p, const vx_choice& ch, int64_t batch, int64_t
 }
 
 vx_status prepare_kernels(const vx_plan_s* p) {
+    DeviceGuard g(p->device);   // attributes and the workspace belong to the plan's device
     if (p->in != VX_FP32) {
-        vx_status s = ensure_ws(p);
+        void* w = nullptr;
+        vx_status s = ensure_ws(p, nullptr, &w);   // the legacy stream's workspace
         if (s != VX_OK) return s;
     }
     for (const vx::Rung& r : p->rungs) {
@@ -468,12 +497,9 @@ vx_status prepare_kernels(const vx_plan_s* p) {
 }  // namespace vx
 
 vx_plan_s::~vx_plan_s() {
-    if (ws) {
-        int cur = 0;
-        cudaGetDevice(&cur);
-        cudaSetDevice(ws_device);
-        cudaFree(ws);
-        cudaSetDevice(cur);
+    for (const auto& w : ws) {
+        vx::DeviceGuard g(w.device);
+        cudaFree(w.ptr);
     }
 }
 
@@ -568,6 +594,16 @@ vx_status vx_gemm_ex(vx_plan_t p, int64_t batch, int64_t M, int64_t N, int64_t K
     vx_status s = check_args(p, batch, M, N, K, A, sA, B, sB, C, sC);
     if (s != VX_OK) return s;
     if (M == 0) return VX_OK;
+    if (p->device >= 0) {
+        // kernel attributes and workspaces were set up for the plan's device; launching
+        // there from another current device would fault or fail (ABI)
+        int cur = -1;
+        if (cudaGetDevice(&cur) != cudaSuccess || cur != p->device) {
+            cudaGetLastError();
+            set_error("current device %d != the plan's device %d", cur, p->device);
+            return VX_ERR_INVALID;
+        }
+    }
     vx_choice ch;
     s = select_choice(p, batch, M, N, force_rung, force_split, &ch);
     if (s != VX_OK) return s;

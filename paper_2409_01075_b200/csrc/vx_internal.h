@@ -76,9 +76,12 @@ struct vx_plan_s {
     static constexpr int64_t kMemo = 16384;
     std::vector<vx_choice> memo;
     std::unique_ptr<std::atomic<uint8_t>[]> memo_state;
-    // stream-K workspace (device): sm_count partial slots of 128 x 256 fp32 + flags
-    void* ws = nullptr;
-    int ws_device = -1;
+    // stream-K workspaces (device): one per (device, stream) the plan launches stream-K on,
+    // each sm_count partial slots of 128 x 256 fp32 + sm_count ready flags.  A workspace is
+    // only ever used by launches on its own stream, which the stream serialises, so
+    // concurrent vx_gemm calls with one plan on different streams never share slots/flags.
+    struct Workspace { void* stream; int device; void* ptr; };
+    std::vector<Workspace> ws;
     std::mutex ws_mu;
     ~vx_plan_s();
 };

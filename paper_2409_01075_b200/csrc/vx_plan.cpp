@@ -427,6 +427,15 @@ vx_status vx_plan_ex(int64_t N, int64_t K, vx_dtype in, vx_dtype out, vx_blayout
         desc->max_active_clusters[0] <= 0) {
         set_error("invalid device descriptor"); return VX_ERR_INVALID;
     }
+    // resident clusters of size c can never exceed sm_count / c: the stream-K workspace has
+    // sm_count slots and its flag spin-wait relies on every CTA of the grid being resident
+    for (int i = 0; i < 4; ++i)
+        if (desc->max_active_clusters[i] < 0 ||
+            (int64_t)desc->max_active_clusters[i] * (1 << i) > desc->sm_count) {
+            set_error("invalid device descriptor: max_active_clusters[%d]=%d exceeds sm_count/%d",
+                      i, desc->max_active_clusters[i], 1 << i);
+            return VX_ERR_INVALID;
+        }
     std::unique_ptr<vx_plan_s> p(new (std::nothrow) vx_plan_s());
     if (!p) return VX_ERR_OOM;
     p->N = N; p->K = K; p->in = in; p->out = out; p->bl = bl; p->desc = *desc; p->device = -1;

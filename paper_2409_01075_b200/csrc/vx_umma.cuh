@@ -68,7 +68,9 @@ struct UmmaParams {
     int* flags;                 // stream-K slot-ready flags [gridDim.x] (0 between launches)
     int kdouble;                // 1: two-chunk loads (tmP2 / tmQ2) fill two adjacent ring
                                 // stages with one TMA box per operand (K % 64 == 0, K-major
-                                // P and Q, non-pair, unpacked; DESIGN.md 4.1 "deep-K units")
+                                // P and Q, unpacked; rings of >= 6 stages, >= 8 for pair
+                                // rungs, whose two-chunk boxes use the .cta_group::2 form;
+                                // DESIGN.md 4.1 "deep-K units")
 };
 
 // ---- work assignment (the L3 schedule of the rung) ---------------------------------------

@@ -110,3 +110,15 @@ def test_missing_library_fails_loudly(tmp_path):
     r = subprocess.run([sys.executable, "-c", "import paper_2409_01075_b200"], cwd=tmp_path,
                        capture_output=True, text=True)
     assert r.returncode != 0 and "libvx.so not built" in r.stderr
+
+
+def test_descriptor_with_impossible_residency_rejected():
+    """A descriptor claiming more resident clusters of size c than sm_count / c is refused:
+    the stream-K workspace has sm_count slots and its flag wait needs the whole grid
+    resident."""
+    for i, bad in ((0, 149), (1, 75), (2, 38), (3, 19)):
+        d = _desc()
+        d.max_active_clusters[i] = bad
+        with pytest.raises(vx.VxError) as e:
+            vx.Plan(4096, 4096, "bf16", "bf16", "nk", desc=d)
+        assert e.value.status == 1

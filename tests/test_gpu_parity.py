@@ -423,3 +423,44 @@ def test_gemv_a_in_smem_long_k():
                 if M <= r["bm"]:
                     got, _ = _run(p, A, B, force=(r["rung_id"], 1))
                     assert np.array_equal(got, want), (K, M, r["bm"])
+
+
+def test_streamk_concurrent_streams_one_plan():
+    """vx.h thread-safety contract: one plan, stream-K launches interleaved on two streams
+    with no synchronisation between them.  Each stream has its own partial workspace and
+    flags, so both results are exact; with a shared workspace the consumers
+    would add each other's partials or clear each other's flags."""
+    vx = vxmod()
+    N, K = 1024, 4096
+    p = vx.Plan(N, K, "bf16", "fp32", "nk")
+    sk = [(r["rung_id"], 0) for r in p.dump()["rungs"] if 0 in r["splits"] and r["family"] != 3]
+    assert sk
+    M = 300
+    ins = [synth.gemm_inputs(M, N, K, "bf16", "nk", kind="int", seed=500 + j) for j in range(2)]
+    want = [oracle.gemm(A, B, "nk") for A, B in ins]
+    dev = [(A.cuda(), B.cuda()) for A, B in ins]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    for force in sk:
+        outs = [[torch.empty((M, N), dtype=torch.float32, device="cuda") for _ in range(8)]
+                for _ in range(2)]
+        torch.cuda.synchronize()
+        for i in range(8):
+            for j in range(2):
+                with torch.cuda.stream(streams[j]):
+                    p.gemm(dev[j][0], dev[j][1], out=outs[j][i], force=force)
+        torch.cuda.synchronize()
+        for j in range(2):
+            for i in range(8):
+                assert np.array_equal(outs[j][i].cpu().double().numpy(), want[j]), (force, j, i)
+
+
+def test_batched_gemm_rejects_unbatched_b():
+    """A [batch, M, K] with a 2-D B would make the C call read batch*N*K elements of B: the
+    binding refuses it instead of reading past the end."""
+    vx = vxmod()
+    p = vx.Plan(0, 64, "bf16", "fp32", "nk")
+    Q = torch.zeros((4, 16, 64), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(ValueError):
+        p.gemm(Q, torch.zeros((16, 64), dtype=torch.bfloat16, device="cuda"))
+    with pytest.raises(ValueError):
+        p.gemm(Q, torch.zeros((3, 16, 64), dtype=torch.bfloat16, device="cuda"))
