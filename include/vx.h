@@ -103,16 +103,20 @@ typedef struct {
  * strategy table), the split of the reduction loop, and the launch geometry. */
 typedef struct {
     int32_t rung_id;  /* index into the plan's strategy table (vx_plan_dump order)          */
-    int32_t split;    /* K-loop split s (cluster of s CTAs reduces through DSMEM); 1 = none */
-    int32_t family;   /* 0 tcgen05, 1 tcgen05 with A/B swapped, 2 fp32 SIMT                 */
+    int32_t split;    /* K-loop schedule: 1 = persistent CTAs over whole-K tiles; s > 1 =
+                         split-K over a cluster of s CTAs reducing through DSMEM; 0 =
+                         stream-K over (tile, k-block) units (R19)                          */
+    int32_t family;   /* 0 tcgen05, 1 tcgen05 with A/B swapped, 2 fp32 SIMT, 3 CUDA-core
+                         GEMV (adaptive backend, R20)                                       */
     int32_t swap;
     int32_t bm, bn;   /* CTA tile on the (UMMA-M, UMMA-N) axes                              */
     int32_t stages;   /* shared-memory pipeline depth                                      */
     int32_t tiles_m;  /* tiles along the UMMA-M axis (M, or N when swapped)                */
     int32_t tiles_n;  /* tiles along the UMMA-N axis                                        */
     int32_t grid;     /* CTAs launched                                                      */
-    int32_t cluster;  /* cluster size (== split)                                            */
-    int32_t reserved;
+    int32_t cluster;  /* CTAs per cluster: split s (DSMEM split-K), 2 (cta_group::2 pair),
+                         mc (TMA-multicast cluster) or 1                                    */
+    int32_t mc;       /* TMA-multicast cluster size sharing the A tile (1 = no multicast)   */
     int64_t cost;     /* predicted cycles, Eq. 4 (integer)                   */
 } vx_choice;
 

@@ -134,12 +134,17 @@ EPI_STAGING = 32768                              # epilogue: 4 warps x 2 x 4 KB 
 CLUSTER_MAX = 8                                  # portable cluster size
 
 # kernels that exist in the library (the "implemented" filter, R6):
-#   family 0: tcgen05, A-tile on the UMMA-M axis: cta_group::1 BM=128, BN in {64,128,256};
+#   family 0: tcgen05, A-tile on the UMMA-M axis: cta_group::1 BM=128, BN in {64,128,192,256};
 #             cta_group::2 pairs BM=256, BN in {128,256}
-#   family 1: same kernel with A/B swapped (N on UMMA-M, M on UMMA-N; BN in {16,32,64,128})
+#   family 1: same kernel with A/B swapped (N on UMMA-M, M on UMMA-N; BN in
+#             {16,32,64,128,192,256})
 #   family 2: fp32 SIMT FFMA (BM, BN, TM, TN) in {(32,32,2,4),(64,64,4,4),(128,64,8,4)}
-IMPL_TC = {(0, 128, 64), (0, 128, 128), (0, 128, 256), (0, 256, 128), (0, 256, 256),
-           (1, 128, 16), (1, 128, 32), (1, 128, 64), (1, 128, 128)}
+IMPL_TC = {(0, 128, 64), (0, 128, 128), (0, 128, 192), (0, 128, 256), (0, 256, 128),
+           (0, 256, 256), (1, 128, 16), (1, 128, 32), (1, 128, 64), (1, 128, 128),
+           (1, 128, 192), (1, 128, 256)}
+# TMA-multicast cluster kernels: (family, bm, bn, mc), mc CTAs sharing the A tile
+IMPL_MC = {(0, 128, 128, 2), (0, 128, 256, 2), (1, 128, 32, 2), (1, 128, 64, 2), (1, 128, 64, 4)}
+MC_SIZES = (1, 2, 4)
 SIMT_TILES = ((32, 32, 2, 4), (64, 64, 4, 4), (128, 64, 8, 4))
 SIMT_BK = 16
 FAMILY_NAMES = {0: "umma", 1: "umma_swap", 2: "simt", 3: "gemv"}
@@ -204,28 +209,40 @@ def build_table(K: int, in_dtype: str, out_dtype: str, desc: dict, b_layout: str
         for (bm, bn, bk, S, st) in l2:
             cg = 2 if bm == 256 else 1
             for swap in (0, 1):
-                if (swap, bm, bn) not in IMPL_TC or st != 2:
-                    continue
                 if cg == 2 and swap:      # cta_group::2 pair rungs are non-swapped
                     continue
                 stage_bytes = (bm // cg + bn // cg) * bk * in_b
-                splits = []
-                for s in SPLITS:
-                    if kb % s != 0 or s * cg > CLUSTER_MAX:
+                for mc in MC_SIZES:
+                    # L3 multicast cluster of mc CTAs sharing the A tile: implemented kernel,
+                    # whole 8-row swizzle atoms per CTA share, unpacked B
+                    if st != 2:
                         continue
-                    if s > 1 and (cg > 1 or bm * (bn + 4) * 4 > S * stage_bytes):
+                    if mc == 1 and (swap, bm, bn) not in IMPL_TC:
                         continue
-                    splits.append(s)
-                splits.append(0)          # stream-K schedule over (tile, k-block) units (R19)
-                rungs.append({"family": swap, "cg": cg, "um": bm, "un": bn, "acc_stages": st,
-                              "bm": bm, "bn": bn, "bk": bk, "stages": S, "swap": swap,
-                              "splits": splits})
+                    if mc > 1 and ((swap, bm, bn, mc) not in IMPL_MC or cg > 1
+                                   or (bn if swap else bm) // mc % 8 != 0
+                                   or b_layout == "packed"):
+                        continue
+                    if mc > 1:
+                        splits = [1]      # multicast clusters run the persistent schedule
+                    else:
+                        splits = []
+                        for s in SPLITS:
+                            if kb % s != 0 or s * cg > CLUSTER_MAX:
+                                continue
+                            if s > 1 and (cg > 1 or bm * (bn + 4) * 4 > S * stage_bytes):
+                                continue
+                            splits.append(s)
+                        splits.append(0)  # stream-K schedule over (tile, k-block) units (R19)
+                    rungs.append({"family": swap, "cg": cg, "um": bm, "un": bn, "acc_stages": st,
+                                  "bm": bm, "bn": bn, "bk": bk, "stages": S, "swap": swap,
+                                  "mc": mc, "splits": splits})
         # adaptive backend (R20): CUDA-core rungs join the same argmin
         if b_layout != "packed":
             for mt in GEMV_MT:
                 rungs.append({"family": 3, "cg": 1, "um": 1, "un": 1, "acc_stages": 1,
                               "bm": mt, "bn": GEMV_COLS, "bk": GEMV_BK, "stages": 1, "swap": 0,
-                              "splits": [1]})
+                              "mc": 1, "splits": [1]})
         counts = {"l0": len(l0), "l1": len(l1), "l2": len(l2), "l3": len(rungs)}
     elif in_dtype == "fp32":
         # CUDA-core mode: L0 = FFMA thread tiles, L2 = CTA tiles
@@ -243,12 +260,12 @@ def build_table(K: int, in_dtype: str, out_dtype: str, desc: dict, b_layout: str
         for (bm, bn, bk, tm, tn) in l2:
             rungs.append({"family": 2, "cg": 1, "um": tm, "un": tn, "acc_stages": 1,
                           "bm": bm, "bn": bn, "bk": bk, "stages": 2, "swap": 0,
-                          "splits": [1]})
+                          "mc": 1, "splits": [1]})
         counts = {"l0": len(l0), "l1": len(l0), "l2": len(l2), "l3": len(rungs)}
     else:
         raise ValueError(in_dtype)
-    # deterministic rung ids (R13): lexicographic on (family, bm, bn, stages, swap)
-    rungs.sort(key=lambda r: (r["family"], r["bm"], r["bn"], r["stages"], r["swap"]))
+    # deterministic rung ids (R13): lexicographic on (family, bm, bn, stages, swap, mc)
+    rungs.sort(key=lambda r: (r["family"], r["bm"], r["bn"], r["stages"], r["swap"], r["mc"]))
     for i, r in enumerate(rungs):
         r["rung_id"] = i
     return {"K": K, "in": in_dtype, "out": out_dtype, "levels": counts, "rungs": rungs}
@@ -260,7 +277,10 @@ def build_table(K: int, in_dtype: str, out_dtype: str, desc: dict, b_layout: str
 
 def _calib_for(rung: dict, calib: dict) -> dict:
     fam = FAMILY_NAMES[rung["family"]]
-    key = "%s_%dx%d" % (fam, rung["bm"], rung["bn"])
+    if rung.get("mc", 1) > 1:
+        key = "%s_mc%d_%dx%d" % (fam, rung["mc"], rung["bm"], rung["bn"])
+    else:
+        key = "%s_%dx%d" % (fam, rung["bm"], rung["bn"])
     return calib["rungs"][key]
 
 
@@ -290,11 +310,17 @@ def rung_cost(rung: dict, s: int, batch: int, M: int, N: int, K: int,
         return _streamk_cost(rung, batch, M, N, K, mt, nt, tm, tn, tiles, kb, in_b, out_b,
                              desc, calib, cal)
     trips = kb // s                                   # sizeof(TemporalLoop) at CTA level (R8)
-    W = tiles * s * rung["cg"]                        # sizeof(ParallelLoop) in CTAs
+    # a multicast cluster covers mc consecutive tiles along the axis that does
+    # not share the A tile; the tile count is padded to whole clusters
+    mc = rung.get("mc", 1)
+    tm_c = ceil_div(tm, mc) * mc if (mc > 1 and rung["swap"]) else tm
+    tn_c = ceil_div(tn, mc) * mc if (mc > 1 and not rung["swap"]) else tn
+    W = batch * tm_c * tn_c * s * rung["cg"]          # sizeof(ParallelLoop) in CTAs
     if rung["family"] == 2:
         slots = simt_slots(rung, desc)
     else:
-        slots = desc["max_active_clusters"][str(s * rung["cg"])] * s * rung["cg"]
+        csz = s * rung["cg"] * mc                     # CTAs per cluster
+        slots = desc["max_active_clusters"][str(csz)] * csz
     F = parallel_factor(W, slots)                     # Eq. 3 (|HardwareUnit| = slots, R9)
     active = min(W, slots)
     if rung["family"] == 2:
@@ -303,8 +329,11 @@ def rung_cost(rung: dict, s: int, batch: int, M: int, N: int, K: int,
         l_smem = t_load((bm + bn) * bk * in_b * occ, cal["l2s_milli"])
     else:
         inner = t_load(bm * bn * bk, cal["mac_milli"])          # Cost_{L-1}, empirical tier
-        # rows past M / N are zero-filled by TMA without memory traffic (R10)
-        l_smem = t_load((min(bm, mt) + min(bn, nt)) * bk * in_b, cal["l2s_milli"])
+        # rows past M / N are zero-filled by TMA without memory traffic (R10); in a multicast
+        # cluster each CTA loads 1/mc of the shared A tile (mc_A)
+        p_rows = bm // mc if (mc > 1 and not rung["swap"]) else min(bm, mt)
+        q_rows = bn // mc if (mc > 1 and rung["swap"]) else min(bn, nt)
+        l_smem = t_load((p_rows + q_rows) * bk * in_b, cal["l2s_milli"])
     # HBM share of one k-step: the grid's unique operand bytes leave HBM once, spread over
     # F waves x trips k-steps that all run at the chip bandwidth (R10)
     uniq = in_b * batch * K * (mt + nt)
@@ -327,7 +356,7 @@ def rung_cost(rung: dict, s: int, batch: int, M: int, N: int, K: int,
         cost = level_cost(F, T) + cal["fixed"] + (calib["fixed_cluster"] if s > 1 else 0)
     return {"cost": cost, "tiles_m": tm, "tiles_n": tn, "tiles": tiles, "F": F,
             "grid": W if s > 1 or rung["family"] == 2 else min(W, slots),
-            "padded_work": batch * tm * bm * tn * bn}
+            "padded_work": batch * tm_c * bm * tn_c * bn}
 
 
 def _gemv_cost(rung, batch, M, N, K, in_b, out_b, desc, calib, cal):
@@ -409,4 +438,4 @@ def select(table: dict, batch: int, M: int, N: int, K: int, desc: dict, calib: d
     key, r, s, c = best
     return {"rung_id": r["rung_id"], "split": s, "tiles_m": c["tiles_m"],
             "tiles_n": c["tiles_n"], "grid": c["grid"], "cost": c["cost"],
-            "swap": r["swap"], "bm": r["bm"], "bn": r["bn"]}
+            "swap": r["swap"], "bm": r["bm"], "bn": r["bn"], "mc": r.get("mc", 1)}

@@ -62,10 +62,10 @@ class DeviceDesc(ctypes.Structure):
 class Choice(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in ("rung_id", "split", "family", "swap", "bm", "bn",
                                               "stages", "tiles_m", "tiles_n", "grid", "cluster",
-                                              "reserved")] + [("cost", ctypes.c_int64)]
+                                              "mc")] + [("cost", ctypes.c_int64)]
 
     def as_dict(self) -> dict:
-        return {n: getattr(self, n) for n, _ in self._fields_ if n != "reserved"}
+        return {n: getattr(self, n) for n, _ in self._fields_}
 
 
 def _load():

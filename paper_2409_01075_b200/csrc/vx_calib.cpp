@@ -38,6 +38,16 @@ static const RungCalib kRungs[] = {
     {"umma_swap_128x32", 1000000, 28993, 8000, 4531},
     {"umma_swap_128x64", 1000000, 42147, 512000, 5892},
     {"umma_swap_128x128", 1449009, 160000, 8000, 726},
+    // BN = 192 / swapped BN = 192, 256 (tile-boundary cliffs, R6): provisional constants
+    {"umma_128x192", 1600000, 100000, 32000, 800},
+    {"umma_swap_128x192", 1600000, 100000, 32000, 800},
+    {"umma_swap_128x256", 1672861, 84000, 32000, 800},
+    // TMA-multicast clusters: provisional = the unicast rung's constants
+    {"umma_mc2_128x128", 1442773, 145125, 16764, 1203},
+    {"umma_mc2_128x256", 1672861, 84000, 512000, 500},
+    {"umma_swap_mc2_128x32", 1000000, 28993, 8000, 4531},
+    {"umma_swap_mc2_128x64", 1000000, 42147, 512000, 5892},
+    {"umma_swap_mc4_128x64", 1000000, 42147, 512000, 5892},
     {"gemv_1x8", 4328, 63578, 16000, 2628},
     {"gemv_2x8", 8000, 74202, 1000, 3062},
     {"gemv_4x8", 8762, 64524, 1000, 2428},

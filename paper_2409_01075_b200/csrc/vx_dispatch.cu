@@ -30,11 +30,21 @@ static const bool g_pdl = [] {                 // VX_PDL=0 disables programmatic
 }();
 
 // ---- instantiated kernels (the "implemented" filter of the strategy table, R6) -----------
-bool kernel_available(int family, int bm, int bn) {
+// TMA-multicast cluster rungs: non-swapped 128 x BN tiles sharing the A (= P)
+// tile over 2 CTAs; swapped tiles sharing the A (= Q) tile over 2 or 4 CTAs
+static bool mc_available(int family, int bm, int bn, int mc) {
+    if (family == kUmma) return mc == 2 && bm == 128 && (bn == 128 || bn == 256);
+    if (family == kUmmaSwap) return bm == 128 && ((mc == 2 && (bn == 32 || bn == 64)) || (mc == 4 && bn == 64));
+    return false;
+}
+
+bool kernel_available(int family, int bm, int bn, int mc) {
+    if (mc != 1) return mc_available(family, bm, bn, mc);
     if (family == kUmma)
-        return (bm == 128 && (bn == 64 || bn == 128 || bn == 256)) ||
+        return (bm == 128 && (bn == 64 || bn == 128 || bn == 192 || bn == 256)) ||
                (bm == 256 && (bn == 128 || bn == 256));     // cta_group::2 pair rungs
-    if (family == kUmmaSwap) return bm == 128 && (bn == 16 || bn == 32 || bn == 64 || bn == 128);
+    if (family == kUmmaSwap)
+        return bm == 128 && (bn == 16 || bn == 32 || bn == 64 || bn == 128 || bn == 192 || bn == 256);
     if (family == kSimt) return (bm == 32 && bn == 32) || (bm == 64 && bn == 64) || (bm == 128 && bn == 64);
     if (family == kGemv) return (bm == 1 || bm == 2 || bm == 4 || bm == 8) && bn == kGemvCols;
     return false;
@@ -58,7 +68,21 @@ static UmmaFn pick_pair(bool b_mn) {
                 : (UmmaFn)vx_umma_kernel<BN, false, false, false, true>;
 }
 
-static UmmaFn umma_fn(int family, int bm, int bn, bool b_mn) {
+template <int BN, bool SWAP, int MC>
+static UmmaFn pick_mc(bool b_mn) {
+    if (SWAP) return b_mn ? (UmmaFn)vx_umma_kernel<BN, true, true, false, false, MC>
+                          : (UmmaFn)vx_umma_kernel<BN, true, false, false, false, MC>;
+    return b_mn ? (UmmaFn)vx_umma_kernel<BN, false, false, true, false, MC>
+                : (UmmaFn)vx_umma_kernel<BN, false, false, false, false, MC>;
+}
+
+static UmmaFn umma_fn(int family, int bm, int bn, bool b_mn, int mc = 1) {
+    if (mc > 1) {
+        if (!mc_available(family, bm, bn, mc)) return nullptr;
+        if (family == kUmma) return bn == 128 ? pick_mc<128, false, 2>(b_mn) : pick_mc<256, false, 2>(b_mn);
+        if (mc == 4) return pick_mc<64, true, 4>(b_mn);
+        return bn == 32 ? pick_mc<32, true, 2>(b_mn) : pick_mc<64, true, 2>(b_mn);
+    }
     if (family == kUmma && bm == 256) {
         switch (bn) {
         case 128: return pick_pair<128>(b_mn);
@@ -70,6 +94,7 @@ static UmmaFn umma_fn(int family, int bm, int bn, bool b_mn) {
         switch (bn) {
         case 64: return pick_mn<64, false>(b_mn);
         case 128: return pick_mn<128, false>(b_mn);
+        case 192: return pick_mn<192, false>(b_mn);
         case 256: return pick_mn<256, false>(b_mn);
         }
     } else if (family == kUmmaSwap) {
@@ -78,6 +103,8 @@ static UmmaFn umma_fn(int family, int bm, int bn, bool b_mn) {
         case 32: return pick_mn<32, true>(b_mn);
         case 64: return pick_mn<64, true>(b_mn);
         case 128: return pick_mn<128, true>(b_mn);
+        case 192: return pick_mn<192, true>(b_mn);
+        case 256: return pick_mn<256, true>(b_mn);
         }
     }
     return nullptr;
@@ -359,7 +386,8 @@ vx_status launch(const vx_plan_s* p, const vx_choice& ch, int64_t batch, int64_t
     const bool swap = r.swap != 0;
     const bool b_mn = p->bl == VX_B_KN;
     const bool pair = r.cg == 2;
-    UmmaFn fn = umma_fn(r.family, r.bm, r.bn, b_mn);
+    const int mc = r.mc;
+    UmmaFn fn = umma_fn(r.family, r.bm, r.bn, b_mn, mc);
     if (!fn) { set_error("no tcgen05 kernel for rung %d", r.rung_id); return VX_ERR_UNSUPPORTED; }
     const int64_t smem = umma_smem_bytes(r.bm, r.bn, r.stages);
     vx_status s = ensure_attr((const void*)fn, smem);
@@ -367,7 +395,9 @@ vx_status launch(const vx_plan_s* p, const vx_choice& ch, int64_t batch, int64_t
 
     // tensor maps: A [batch][M][K] K-major; B [batch][N][K] (NK) or [batch][K][N] (KN)
     CUtensorMap mapA, mapB;
-    const int a_box = swap ? r.bn : 128;  // A is P (box 128 rows) or Q (box BN rows)
+    // A is P (box 128 rows) or Q (box BN rows); in a multicast cluster each CTA loads (and
+    // multicasts) 1/mc of A's rows
+    const int a_box = (swap ? r.bn : 128) / mc;
     s = make_map(&mapA, A, p->in, K, M, batch, K, batch > 1 ? sA : M * K, 64, a_box);
     if (s != VX_OK) return s;
     if (p->bl == VX_B_PACKED) {
@@ -385,7 +415,10 @@ vx_status launch(const vx_plan_s* p, const vx_choice& ch, int64_t batch, int64_t
     prm.N = (int)N;
     prm.tiles_p = ch.tiles_m;
     prm.tiles_q = ch.tiles_n;
-    prm.num_tiles = (int)(batch * (int64_t)ch.tiles_m * ch.tiles_n);
+    // multicast clusters walk cluster tiles (mc tiles along the axis not sharing A)
+    prm.mc = mc;
+    prm.num_tiles = (int)(batch * (mc > 1 && swap ? cdiv(ch.tiles_m, mc) : (int64_t)ch.tiles_m) *
+                          (mc > 1 && !swap ? cdiv(ch.tiles_n, mc) : (int64_t)ch.tiles_n));
     prm.kb_total = (int)cdiv(K, kBkTc);
     prm.splits = ch.split > 0 ? ch.split : 1;
     prm.streamk = ch.split == 0;
@@ -413,7 +446,7 @@ vx_status launch(const vx_plan_s* p, const vx_choice& ch, int64_t batch, int64_t
     // measured, 128 x 256 (4 stages) up to 1.17x slower, pair 256 x 256 (6 stages) 1.03x
     // slower, pair 256 x 128 (8 stages) 0.86-0.90x; VX_DEBUG_FLAGS bit 4096 turns them off
     // (A/B timing only)
-    prm.kdouble = (!b_mn && p->bl != VX_B_PACKED && K % 64 == 0 && K >= 128 &&
+    prm.kdouble = (!b_mn && p->bl != VX_B_PACKED && K % 64 == 0 && K >= 128 && mc == 1 &&
                    r.stages >= (pair ? 8 : 6) && !(g_dbg & 4096)) ? 1 : 0;
     CUtensorMap mapA2, mapB2;
     if (prm.kdouble) {
@@ -450,9 +483,9 @@ vx_status launch(const vx_plan_s* p, const vx_choice& ch, int64_t batch, int64_t
     cfg.stream = st;
     cudaLaunchAttribute attr[2];
     unsigned na = 0;
-    if (ch.split > 1 || pair) {   // split-K cluster or CTA pair (split 0 = stream-K)
+    if (ch.split > 1 || pair || mc > 1) {   // split-K cluster, CTA pair or multicast cluster
         attr[na].id = cudaLaunchAttributeClusterDimension;
-        attr[na].val.clusterDim.x = (unsigned)(pair ? 2 : ch.split);
+        attr[na].val.clusterDim.x = (unsigned)(pair ? 2 : mc > 1 ? mc : ch.split);
         attr[na].val.clusterDim.y = 1;
         attr[na].val.clusterDim.z = 1;
         ++na;
@@ -486,7 +519,7 @@ vx_status prepare_kernels(const vx_plan_s* p) {
     }
     for (const vx::Rung& r : p->rungs) {
         if (r.family == kSimt) continue;
-        UmmaFn fn = umma_fn(r.family, r.bm, r.bn, p->bl == VX_B_KN);
+        UmmaFn fn = umma_fn(r.family, r.bm, r.bn, p->bl == VX_B_KN, r.mc);
         if (!fn) continue;
         vx_status s = ensure_attr((const void*)fn, umma_smem_bytes(r.bm, r.bn, r.stages));
         if (s != VX_OK) return s;

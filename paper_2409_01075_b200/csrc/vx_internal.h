@@ -37,6 +37,7 @@ struct Rung {
     int32_t bm, bn, bk;  // L2: CTA tile
     int32_t stages;      // L2: SMEM pipeline depth
     int32_t swap;        // L3: operand swap
+    int32_t mc;          // L3: TMA-multicast cluster size sharing the A tile (1 = none)
     std::vector<int32_t> splits;  // L3: admissible K-loop splits
     // calibration (empirical tier), scaled x1000
     int64_t mac_milli, l2s_milli, epi_milli, fixed;

@@ -26,7 +26,7 @@
 
 namespace vx {
 
-bool kernel_available(int family, int bm, int bn);  // vx_dispatch.cu
+bool kernel_available(int family, int bm, int bn, int mc = 1);  // vx_dispatch.cu
 
 static thread_local char g_err[512] = "";
 
@@ -135,19 +135,33 @@ static vx_status build_rungs(vx_plan_s* p) {
             int cg = c.bm == 256 ? 2 : 1;
             for (int swap = 0; swap <= 1; ++swap) {
                 int fam = swap ? kUmmaSwap : kUmma;
-                if (c.st != 2 || !kernel_available(fam, c.bm, c.bn)) continue;
                 if (cg == 2 && swap) continue;      // pair rungs are non-swapped
                 int64_t stage = (int64_t)(c.bm / cg + c.bn / cg) * c.bk * in_b;
-                Rung r{};
-                r.family = fam; r.cg = cg; r.um = c.bm; r.un = c.bn; r.acc_stages = c.st;
-                r.bm = c.bm; r.bn = c.bn; r.bk = c.bk; r.stages = c.S; r.swap = swap;
-                for (int s : {1, 2, 4, 8}) {
-                    if (kb % s != 0 || s * cg > kClusterMax) continue;
-                    if (s > 1 && (cg > 1 || (int64_t)c.bm * (c.bn + 4) * 4 > c.S * stage)) continue;
-                    r.splits.push_back(s);
+                // TMA-multicast clusters of mc CTAs sharing the A tile: the
+                // multicast sub-box (A rows / mc) must be whole 8-row swizzle atoms and a
+                // packed B keeps its own 5-D load path, so multicast needs B unpacked
+                for (int mc : {1, 2, 4}) {
+                    if (c.st != 2 || !kernel_available(fam, c.bm, c.bn, mc)) continue;
+                    if (mc > 1 && (cg > 1 || (swap ? c.bn : c.bm) / mc % 8 != 0 ||
+                                   p->bl == VX_B_PACKED))
+                        continue;
+                    Rung r{};
+                    r.family = fam; r.cg = cg; r.um = c.bm; r.un = c.bn; r.acc_stages = c.st;
+                    r.bm = c.bm; r.bn = c.bn; r.bk = c.bk; r.stages = c.S; r.swap = swap;
+                    r.mc = mc;
+                    if (mc > 1) {
+                        r.splits = {1};     // multicast clusters run the persistent schedule
+                        rungs.push_back(r);
+                        continue;
+                    }
+                    for (int s : {1, 2, 4, 8}) {
+                        if (kb % s != 0 || s * cg > kClusterMax) continue;
+                        if (s > 1 && (cg > 1 || (int64_t)c.bm * (c.bn + 4) * 4 > c.S * stage)) continue;
+                        r.splits.push_back(s);
+                    }
+                    r.splits.push_back(0);  // stream-K over (tile, k-block) units (R19)
+                    rungs.push_back(r);
                 }
-                r.splits.push_back(0);  // stream-K over (tile, k-block) units (R19)
-                rungs.push_back(r);
             }
         }
         // adaptive backend (R20): CUDA-core GEMV-style rungs for tiny M (M <= MT), competing
@@ -158,6 +172,7 @@ static vx_status build_rungs(vx_plan_s* p) {
                 Rung r{};
                 r.family = kGemv; r.cg = 1; r.um = 1; r.un = 1; r.acc_stages = 1;
                 r.bm = mt; r.bn = kGemvColsPerCta; r.bk = kGemvBk; r.stages = 1; r.swap = 0;
+                r.mc = 1;
                 r.splits = {1};
                 rungs.push_back(r);
             }
@@ -178,6 +193,7 @@ static vx_status build_rungs(vx_plan_s* p) {
             Rung r{};
             r.family = kSimt; r.cg = 1; r.um = t.tm; r.un = t.tn; r.acc_stages = 1;
             r.bm = t.bm; r.bn = t.bn; r.bk = kSimtBk; r.stages = 2; r.swap = 0;
+            r.mc = 1;
             r.splits = {1};
             rungs.push_back(r);
         }
@@ -185,13 +201,14 @@ static vx_status build_rungs(vx_plan_s* p) {
     }
     // deterministic ids (R13)
     std::sort(rungs.begin(), rungs.end(), [](const Rung& a, const Rung& b) {
-        return std::tie(a.family, a.bm, a.bn, a.stages, a.swap) <
-               std::tie(b.family, b.bm, b.bn, b.stages, b.swap); });
+        return std::tie(a.family, a.bm, a.bn, a.stages, a.swap, a.mc) <
+               std::tie(b.family, b.bm, b.bn, b.stages, b.swap, b.mc); });
     for (size_t i = 0; i < rungs.size(); ++i) {
         Rung& r = rungs[i];
         r.rung_id = (int32_t)i;
         char key[64];
-        snprintf(key, sizeof key, "%s_%dx%d", family_name(r.family), r.bm, r.bn);
+        if (r.mc > 1) snprintf(key, sizeof key, "%s_mc%d_%dx%d", family_name(r.family), r.mc, r.bm, r.bn);
+        else snprintf(key, sizeof key, "%s_%dx%d", family_name(r.family), r.bm, r.bn);
         const RungCalib* c = calib_lookup(key);
         if (!c) { set_error("no calibration for rung %s", key); return VX_ERR_UNSUPPORTED; }
         r.mac_milli = c->mac_milli; r.l2s_milli = c->l2s_milli;
@@ -245,7 +262,7 @@ static void rung_cost(const vx_plan_s* p, const Rung& r, int s, int64_t batch, i
         o->rung_id = r.rung_id; o->split = 1; o->family = r.family; o->swap = 0;
         o->bm = r.bm; o->bn = r.bn; o->stages = r.stages;
         o->tiles_m = 1; o->tiles_n = (int32_t)cdiv(N, bn); o->grid = (int32_t)tiles_g;
-        o->cluster = 1; o->reserved = 0;
+        o->cluster = 1; o->mc = 1;
         o->cost = Fg * eq2(tl_g, trips_g, inner_g, ts_g) + r.fixed;
         return;
     }
@@ -268,12 +285,17 @@ static void rung_cost(const vx_plan_s* p, const Rung& r, int s, int64_t batch, i
         o->rung_id = r.rung_id; o->split = 0; o->family = r.family; o->swap = r.swap;
         o->bm = r.bm; o->bn = r.bn; o->stages = r.stages;
         o->tiles_m = (int32_t)tm; o->tiles_n = (int32_t)tn; o->grid = (int32_t)(G * r.cg);
-        o->cluster = r.cg; o->reserved = 0;
+        o->cluster = r.cg; o->mc = 1;
         o->cost = std::max(tm_, segs * st) + st + fix + r.fixed;
         return;
     }
     const int64_t trips = kb / s;            // sizeof(TemporalLoop) at the CTA level (R8)
-    const int64_t W = tiles * s * r.cg;      // sizeof(ParallelLoop) in CTAs at the grid level
+    // multicast clusters work on cluster tiles: mc consecutive tiles along the
+    // axis that does NOT share the A tile (Q for non-swapped, P for swapped rungs)
+    const int64_t mc = r.mc;
+    const int64_t tm_c = (mc > 1 && r.swap) ? cdiv(tm, mc) * mc : tm;
+    const int64_t tn_c = (mc > 1 && !r.swap) ? cdiv(tn, mc) * mc : tn;
+    const int64_t W = batch * tm_c * tn_c * s * r.cg;   // sizeof(ParallelLoop) in CTAs
     int64_t slots;
     if (r.family == kSimt) {
         int64_t threads = (bm / r.um) * (bn / r.un);
@@ -282,8 +304,9 @@ static void rung_cost(const vx_plan_s* p, const Rung& r, int s, int64_t batch, i
                                         d.max_threads_per_sm / threads), 32);
         slots = (int64_t)d.sm_count * std::max<int64_t>(occ, 1);
     } else {
-        int ci = s * r.cg == 1 ? 0 : s * r.cg == 2 ? 1 : s * r.cg == 4 ? 2 : 3;
-        slots = (int64_t)d.max_active_clusters[ci] * s * r.cg;
+        const int64_t csz = s * r.cg * mc;   // CTAs per cluster
+        int ci = csz == 1 ? 0 : csz == 2 ? 1 : csz == 4 ? 2 : 3;
+        slots = (int64_t)d.max_active_clusters[ci] * csz;
     }
     const int64_t F = eq3(W, slots);         // Eq. 3, |HardwareUnit| = resident CTAs (R9)
     const int64_t active = std::min(W, slots);
@@ -294,8 +317,11 @@ static void rung_cost(const vx_plan_s* p, const Rung& r, int s, int64_t batch, i
         l_smem = t_move((bm + bn) * bk * in_b * occ, r.l2s_milli);
     } else {
         inner = t_move(bm * bn * bk, r.mac_milli);           // Cost_{L-1}
-        // rows past M / N are zero-filled by TMA without memory traffic (R10)
-        l_smem = t_move((std::min(bm, mt) + std::min(bn, nt)) * bk * in_b, r.l2s_milli);
+        // rows past M / N are zero-filled by TMA without memory traffic (R10); a multicast
+        // cluster's CTA loads only its 1/mc share of the shared A tile (SURVEY C2 mc_A)
+        const int64_t p_rows = (mc > 1 && !r.swap) ? bm / mc : std::min(bm, mt);
+        const int64_t q_rows = (mc > 1 && r.swap) ? bn / mc : std::min(bn, nt);
+        l_smem = t_move((p_rows + q_rows) * bk * in_b, r.l2s_milli);
     }
     const int64_t uniq = (int64_t)in_b * batch * K * (mt + nt);
     const int64_t l_hbm = t_move(uniq, F * trips * cal.hbm_milli);   // R10
@@ -321,13 +347,16 @@ static void rung_cost(const vx_plan_s* p, const Rung& r, int s, int64_t batch, i
     o->tiles_m = (int32_t)tm;
     o->tiles_n = (int32_t)tn;
     o->grid = (int32_t)((s > 1 || r.family == kSimt) ? W : std::min(W, slots));
-    o->cluster = s * r.cg;
-    o->reserved = 0;
+    o->cluster = (int32_t)(s * r.cg * mc);
+    o->mc = (int32_t)mc;
     o->cost = cost;
 }
 
 static inline int64_t padded_work(const vx_choice& c, int64_t batch) {
-    return batch * (int64_t)c.tiles_m * c.bm * (int64_t)c.tiles_n * c.bn;
+    // a multicast cluster pads its tile count to a multiple of mc along the non-shared axis
+    const int64_t tm = (c.mc > 1 && c.swap) ? cdiv(c.tiles_m, c.mc) * c.mc : c.tiles_m;
+    const int64_t tn = (c.mc > 1 && !c.swap) ? cdiv(c.tiles_n, c.mc) * c.mc : c.tiles_n;
+    return batch * tm * c.bm * tn * c.bn;
 }
 
 vx_status select_choice(const vx_plan_s* p, int64_t batch, int64_t M, int64_t N,
@@ -495,9 +524,9 @@ vx_status vx_plan_dump(vx_plan_t p, char* buf, size_t cap, size_t* need) {
         const Rung& r = p->rungs[i];
         snprintf(tmp, sizeof tmp,
                  "%s{\"rung_id\":%d,\"family\":%d,\"cg\":%d,\"um\":%d,\"un\":%d,\"acc_stages\":%d,"
-                 "\"bm\":%d,\"bn\":%d,\"bk\":%d,\"stages\":%d,\"swap\":%d,\"splits\":[",
+                 "\"bm\":%d,\"bn\":%d,\"bk\":%d,\"stages\":%d,\"swap\":%d,\"mc\":%d,\"splits\":[",
                  i ? "," : "", r.rung_id, r.family, r.cg, r.um, r.un, r.acc_stages, r.bm, r.bn,
-                 r.bk, r.stages, r.swap);
+                 r.bk, r.stages, r.swap, r.mc);
         s += tmp;
         for (size_t j = 0; j < r.splits.size(); ++j) {
             snprintf(tmp, sizeof tmp, "%s%d", j ? "," : "", r.splits[j]);

@@ -72,6 +72,18 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const void* tmap, uint64_
         "l"(policy)
         : "memory");
 }
+// 3-D tile load multicast to every CTA of the cluster in `mask`: the box lands at the same
+// shared-memory offset in each destination CTA and its bytes complete_tx on each
+// destination's mbarrier at the same offset (TMA multicast)
+__device__ __forceinline__ void tma_load_3d_mc(void* dst, const void* tmap, uint64_t* bar, int c0,
+                                               int c1, int c2, uint16_t mask, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster.L2::cache_hint"
+        " [%0], [%1, {%2, %3, %4}], [%5], %6, %7;" ::"r"(smem_addr(dst)),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_addr(bar)),
+        "h"(mask), "l"(policy)
+        : "memory");
+}
 // 3-D tile prefetch global -> L2 (no shared-memory destination, no completion).  L2 is
 // the coherence point, so this is safe even while a preceding grid may still write the
 // tile: a later write updates the L2 line.
@@ -230,6 +242,15 @@ __device__ __forceinline__ void umma_f16_pair(uint32_t d_tmem, uint64_t a_desc, 
 __device__ __forceinline__ void umma_commit_pair(uint64_t* bar, uint16_t mask) {
     asm volatile(
         "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_addr(bar)),
+        "h"(mask)
+        : "memory");
+}
+// cta_group::1 commit that arrives on the same-offset mbarrier of every CTA in `mask` (a
+// stage filled by multicast is free only when every CTA of the cluster consumed it)
+__device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
             smem_addr(bar)),
         "h"(mask)
         : "memory");

@@ -66,6 +66,9 @@ struct UmmaParams {
     int bpack;                  // 1: B is VX_B_PACKED (5-D map of 64 x 64 contiguous tiles)
     float* ws;                  // stream-K partial slots [gridDim.x][128][BN] fp32 (plan-owned)
     int* flags;                 // stream-K slot-ready flags [gridDim.x] (0 between launches)
+    int mc;                     // TMA-multicast cluster size (1 = none): MC CTAs share the A
+                                // operand tile (P when non-swapped, Q when swapped); tiles
+                                // and num_tiles then count cluster tiles
     int kdouble;                // 1: two-chunk loads (tmP2 / tmQ2) fill two adjacent ring
                                 // stages with one TMA box per operand (K % 64 == 0, K-major
                                 // P and Q, unpacked; rings of >= 6 stages, >= 8 for pair
@@ -94,6 +97,11 @@ struct WorkIter {
         } else if (p.pair) {
             tile = blockIdx.x >> 1;          // both CTAs of a pair walk the same tiles
             step = gridDim.x >> 1;
+            ka = 0;
+            kn = p.kb_total;
+        } else if (p.mc > 1) {
+            tile = blockIdx.x / p.mc;        // every CTA of a multicast cluster walks the
+            step = gridDim.x / p.mc;         // same cluster tiles in lockstep
             ka = 0;
             kn = p.kb_total;
         } else if (p.splits > 1) {
@@ -179,6 +187,23 @@ __device__ __forceinline__ void decode_tile(int tile, int tiles_p, int tiles_q, 
     const int local = t - group * kGroupP * tiles_q;
     tp = first + local % gsz;
     tq = local / gsz;
+}
+
+// tile of CTA `crank` of a multicast cluster: cluster tile `tile` covers MC consecutive Q
+// tiles sharing one P tile (non-swapped: A = P shared) or MC consecutive P tiles sharing one
+// Q tile (swapped: A = Q shared); the group raster runs over cluster tiles
+template <bool SWAP, int MC>
+__device__ __forceinline__ void decode_ctile(int tile, int tiles_p, int tiles_q, uint32_t crank,
+                                             int& b, int& tp, int& tq) {
+    if (MC == 1) {
+        decode_tile(tile, tiles_p, tiles_q, b, tp, tq);
+    } else if (!SWAP) {
+        decode_tile(tile, tiles_p, (tiles_q + MC - 1) / MC, b, tp, tq);
+        tq = tq * MC + (int)crank;
+    } else {
+        decode_tile(tile, (tiles_p + MC - 1) / MC, tiles_q, b, tp, tq);
+        tp = tp * MC + (int)crank;
+    }
 }
 
 __device__ __forceinline__ uint32_t pack2(float a, float b, int kind) {
@@ -335,12 +360,21 @@ __device__ __forceinline__ void sk_reset(const UmmaParams& p, int c0, int c1, ui
 // PAIR: cta_group::2 rung -- a cluster of 2 CTAs computes a 256 x BN tile; each CTA loads
 // its 128 rows of A and BN/2 rows of B, the leader (rank 0) issues the 256-row MMAs, each
 // CTA's TMEM holds its 128 rows of the accumulator (non-swap, persistent schedule only).
-template <int BN, bool SWAP, bool P_MN, bool Q_MN, bool PAIR = false>
+// MC: TMA-multicast cluster of MC CTAs sharing the A tile (persistent schedule only): each
+// CTA loads 1/MC of the shared tile's rows and multicasts them to the whole cluster; a
+// stage is refilled only when all MC CTAs' MMAs released it (empty barriers count MC).
+template <int BN, bool SWAP, bool P_MN, bool Q_MN, bool PAIR = false, int MC = 1>
 __global__ void __launch_bounds__(kThreads, 1)
     vx_umma_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmQ,
                    const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmP2,
                    const __grid_constant__ CUtensorMap tmQ2, const __grid_constant__ UmmaParams p) {
     static_assert(!PAIR || !SWAP, "pair rungs are non-swapped");
+    static_assert(MC == 1 || !PAIR, "multicast clusters are cta_group::1");
+    static_assert(MC == 1 || (SWAP ? BN / MC : 128 / MC) % 8 == 0,
+                  "multicast sub-boxes are whole 8-row swizzle atoms");
+    constexpr bool MCP = MC > 1 && !SWAP;   // A = P is the multicast operand
+    constexpr bool MCQ = MC > 1 && SWAP;    // A = Q is the multicast operand
+    constexpr uint16_t kMcMask = (uint16_t)((1u << MC) - 1);
     using Cfg = UmmaCfg<BN>;
     constexpr int kP = Cfg::kPBytes;
     constexpr int kQ = PAIR ? Cfg::kQBytes / 2 : Cfg::kQBytes;   // this CTA's B rows
@@ -375,7 +409,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int i = 0; i < S; ++i) {
             ptx::mbar_init(&full[i], 1);
-            ptx::mbar_init(&empty[i], 1);
+            ptx::mbar_init(&empty[i], MC);   // one release per consuming CTA of the cluster
         }
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(&tfull[i], 1);
@@ -392,10 +426,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) cyc_at(p, 28, c);
     }
     ptx::tc_fence_before();
-    if (PAIR) ptx::cluster_sync();   // both CTAs' barriers initialised before any remote use
-    else __syncthreads();
+    if (PAIR || MC > 1) ptx::cluster_sync();   // every CTA's barriers initialised before any
+    else __syncthreads();                      // remote arrive / multicast write
     ptx::tc_fence_after();
     const uint32_t prank = PAIR ? ptx::cluster_ctarank() : 0;   // 0 = pair leader
+    const uint32_t crank = MC > 1 ? ptx::cluster_ctarank() : 0; // rank in a multicast cluster
     const uint32_t tmem_base = *tmem_holder;
     if (threadIdx.x == 0) { trace_at(p, 1); cyc_at(p, 26, cyc_entry); }
     // Programmatic dependent launch: everything up to each role's first global access
@@ -413,7 +448,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             // ===== TMA producers: producer `pid` takes this CTA's k-blocks j % 2 == pid =====
             const int pid = warp == 0 ? 0 : 1;
-            const bool kd = p.kdouble && !P_MN && !Q_MN && !p.bpack;
+            const bool kd = p.kdouble && !P_MN && !Q_MN && !p.bpack && MC == 1;
             const long long cy0 = p.trace ? clock64() : 0;   // trace: setup -> first issue
             const uint64_t pol = (p.dbg & 1024) ? ptx::policy_evict_first()
                                : (p.dbg & 2048) ? ptx::policy_evict_normal()
@@ -431,9 +466,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (waited) return;
                 if (pid == 0 && !(p.dbg & 128) && !p.bpack && !P_MN && !Q_MN) {
                     int b_, tp_, tq_;
-                    decode_tile(tile_, p.tiles_p, p.tiles_q, b_, tp_, tq_);
-                    const int pp = PAIR ? tp_ * 256 + (int)prank * 128 : tp_ * 128;
-                    const int qq = PAIR ? tq_ * BN + (int)prank * (BN / 2) : tq_ * BN;
+                    decode_ctile<SWAP, MC>(tile_, p.tiles_p, p.tiles_q, crank, b_, tp_, tq_);
+                    // this CTA's own rows (its half of a pair, its 1/MC share of the
+                    // multicast operand): the maps' boxes are sized to them
+                    const int pp = PAIR ? tp_ * 256 + (int)prank * 128
+                                 : tp_ * 128 + (MCP ? (int)crank * (128 / MC) : 0);
+                    const int qq = PAIR ? tq_ * BN + (int)prank * (BN / 2)
+                                 : tq_ * BN + (MCQ ? (int)crank * (BN / MC) : 0);
                     const int n = nleft < S ? nleft : S;
                     for (int kb2 = kb_; kb2 < kb_ + n; ++kb2) {
                         ptx::tma_prefetch_3d(&tmP, kb2 * 64, pp, b_);
@@ -449,7 +488,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             int tile, k0, nk;
             while (wi.next(p, tile, k0, nk)) {
                 int b, tp, tq;
-                decode_tile(tile, p.tiles_p, p.tiles_q, b, tp, tq);
+                decode_ctile<SWAP, MC>(tile, p.tiles_p, p.tiles_q, crank, b, tp, tq);
                 if (pid == 0 && j == 0) cyc_at(p, 22, cy0);
                 for (int kb = k0; kb < k0 + nk; ++kb, ++j) {
                     // a unit is one k-block, or two (deep-K) when the next k-block of this
@@ -552,6 +591,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                         for (int a = 0; a < 2; ++a)
                             ptx::tma_load_3d(dP + a * 8192, &tmP, &full[stage], tp * 128 + a * 64,
                                              kb * 64, b, pol);
+                    } else if (MCP) {
+                        // this CTA's 128/MC rows of the shared P tile, into every CTA's stage
+                        ptx::tma_load_3d_mc(dP + crank * (kP / MC), &tmP, &full[stage], kb * 64,
+                                            tp * 128 + (int)crank * (128 / MC), b, kMcMask, pol);
                     } else {
                         ptx::tma_load_3d(dP, &tmP, &full[stage], kb * 64, tp * 128, b, pol);
                     }
@@ -560,6 +603,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                         for (int a = 0; a < BN / 64; ++a)
                             ptx::tma_load_3d(dQ + a * 8192, &tmQ, &full[stage], tq * BN + a * 64,
                                              kb * 64, b, pol);
+                    } else if (MCQ) {
+                        // this CTA's BN/MC rows of the shared Q tile, into every CTA's stage
+                        ptx::tma_load_3d_mc(dQ + crank * (kQ / MC), &tmQ, &full[stage], kb * 64,
+                                            tq * BN + (int)crank * (BN / MC), b, kMcMask, pol);
                     } else {
                         ptx::tma_load_3d(dQ, &tmQ, &full[stage], kb * 64, tq * BN, b, pol);
                     }
@@ -567,6 +614,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
             ptx::grid_dep_launch();  // all loads issued: let the next grid start its prologue
+            if (MC > 1 && pid == 0) {
+                // multicast tail: every CTA's MMA releases this CTA's stages remotely; wait
+                // until each stage's last release has arrived, so no remote arrive can
+                // target this CTA after it passes the final cluster barrier
+                for (int i = 0; i < S; ++i) {
+                    ptx::mbar_wait(&empty[stage], phase ^ 1);
+                    if (++stage == S) { stage = 0; phase ^= 1; }
+                }
+            }
             if (pid == 0) trace_at(p, 2);
         }
     } else if (warp == 1) {
@@ -588,7 +644,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             int stage = 0;
             uint32_t phase = 0;
             int it = 0;
-            const bool kd = p.kdouble && !P_MN && !Q_MN && !p.bpack;
+            const bool kd = p.kdouble && !P_MN && !Q_MN && !p.bpack && MC == 1;
             WorkIter wi(p, rank);
             int tile, k0, nk;
             for (; wi.next(p, tile, k0, nk); ++it) {
@@ -624,8 +680,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                             }
                         }
                         c2 = tr ? clock64() : 0;
-                        // frees the stage (in both CTAs of a pair) when these MMAs finish
+                        // frees the stage (in both CTAs of a pair / every CTA of a multicast
+                        // cluster) when these MMAs finish
                         if (PAIR) ptx::umma_commit_pair(&empty[stage], 3);
+                        else if (MC > 1) ptx::umma_commit_mc(&empty[stage], kMcMask);
                         else ptx::umma_commit(&empty[stage]);
                         if (tr) {
                             const long long c3 = clock64();
@@ -673,7 +731,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const long long U = (long long)p.num_tiles * p.kb_total;
         for (; wi.next(p, tile, k0, nk); ++it) {
             int b, tp, tq;
-            decode_tile(tile, p.tiles_p, p.tiles_q, b, tp, tq);
+            decode_ctile<SWAP, MC>(tile, p.tiles_p, p.tiles_q, crank, b, tp, tq);
             // first P-axis row of this CTA's accumulator rows (a pair splits 256 rows)
             const int prow0 = PAIR ? tp * 256 + (int)prank * 128 : tp * 128;
             // ---- stream-K bookkeeping (before the accumulator wait) ---------------------
@@ -996,8 +1054,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (split) cyc_at(p, 29, cyr);
     }
     ptx::tc_fence_before();
-    if (PAIR) ptx::cluster_sync();   // no CTA of a pair retires while its peer may touch it
-    else __syncthreads();
+    if (PAIR || MC > 1) ptx::cluster_sync();   // no CTA of a cluster retires while a peer may
+    else __syncthreads();                      // still touch its shared memory
     if (warp == 1) {
         __syncwarp();
         ptx::tc_fence_after();

@@ -101,7 +101,11 @@ def test_table_invariants(K):
         foot = r["stages"] * (r["bm"] // cg + r["bn"] // cg) * r["bk"] * 2 + S.SMEM_RESERVE + S.EPI_STAGING
         assert foot <= DESC["smem_optin"] and r["stages"] >= 2
         assert r["acc_stages"] * r["bn"] <= DESC["tmem_cols"]
-        # split-K slices are whole k-blocks
+        # split-K slices are whole k-blocks; multicast clusters are persistent
+        if r["mc"] > 1:
+            assert r["splits"] == [1] and r["cg"] == 1
+            assert (r["bn"] if r["swap"] else r["bm"]) // r["mc"] % 8 == 0   # whole swizzle atoms
+            continue
         assert 1 in r["splits"] and 0 in r["splits"]         # 0 = stream-K (R19)
         assert all(s == 0 or kb % s == 0 for s in r["splits"])
     # sample-free and deterministic: a pure function of (K, dtypes, descriptor)
@@ -141,7 +145,9 @@ def test_zero_padding_on_tile_multiples():
             continue                                   # GEMV rungs cover M <= MT only
         c = S.rung_cost(r, 1, 1, 128 * 40, 256 * 43, 4096, "bf16", "bf16", DESC, CAL)
         mt, nt = (256 * 43, 128 * 40) if r["swap"] else (128 * 40, 256 * 43)
-        if mt % r["bm"] == 0 and nt % r["bn"] == 0:
+        # a multicast cluster also pads its non-shared tile count to a multiple of mc
+        ct = (mt // r["bm"]) if r["swap"] else (nt // r["bn"])
+        if mt % r["bm"] == 0 and nt % r["bn"] == 0 and ct % r["mc"] == 0:
             assert c["padded_work"] == mt * nt
 
 

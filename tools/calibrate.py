@@ -51,7 +51,8 @@ def measure(args):
                     t = time_graph(p, 1, M, N, K, r["rung_id"], s, dev, stream, l2, 3, "nk")
                     out["samples"].append({"M": M, "N": N, "K": K, "rung": r["rung_id"],
                                            "family": r["family"], "bm": r["bm"], "bn": r["bn"],
-                                           "stages": r["stages"], "split": s, "us": t})
+                                           "mc": r.get("mc", 1), "stages": r["stages"],
+                                           "split": s, "us": t})
             print("N=%d K=%d M=%d done" % (N, K, M), flush=True)
     json.dump(out, open(args.out, "w"))
 
@@ -59,6 +60,11 @@ def measure(args):
 # ---- integer model (DESIGN.md 3.3 / R19, the library's arithmetic) --------------------------
 def _cd(a, b):
     return -(-a // b)
+
+
+def calib_key(fam, bm, bn, mc=1):
+    """Calibration-table key of a rung (the library's vx_plan.cpp naming)."""
+    return "%s_mc%d_%dx%d" % (fam, mc, bm, bn) if mc > 1 else "%s_%dx%d" % (fam, bm, bn)
 
 
 def model_us(sm, th, desc, g):
@@ -91,7 +97,10 @@ def model_us(sm, th, desc, g):
     tiles = tm * tn
     kb = _cd(K, bk)
     c = t(bm * bn * bk, mac)
-    ls = t((min(bm, mt) + min(bn, nt)) * bk * 2, l2s)
+    mc = sm.get("mc", 1)                 # TMA-multicast cluster sharing the A tile
+    p_rows = bm // mc if (mc > 1 and not swap) else min(bm, mt)
+    q_rows = bn // mc if (mc > 1 and swap) else min(bn, nt)
+    ls = t((p_rows + q_rows) * bk * 2, l2s)
     if s == 0:   # stream-K (R19), admitted only for <= 3 data-parallel waves
         cgk = 2 if bm == 256 else 1
         if tiles * cgk > 3 * desc["max_active_clusters"][str(cgk)] * cgk:
@@ -109,8 +118,10 @@ def model_us(sm, th, desc, g):
         return cyc / (CLOCK_GHZ * 1e3)
     cg = 2 if bm == 256 else 1
     trips = kb // s
-    W = tiles * s * cg
-    slots = desc["max_active_clusters"][str(s * cg)] * s * cg
+    tm_c = _cd(tm, mc) * mc if (mc > 1 and swap) else tm
+    tn_c = _cd(tn, mc) * mc if (mc > 1 and not swap) else tn
+    W = tm_c * tn_c * s * cg
+    slots = desc["max_active_clusters"][str(s * cg * mc)] * s * cg * mc
     F = _cd(W, slots)
     l = max(ls, t(2 * K * (mt + nt), F * trips * hbm))
     st = max(t(bm * bn * 2, s * epi), t(2 * M * N, F * hbm))
@@ -132,9 +143,9 @@ def fit(args):
     desc = raw["desc"]
     S = raw["samples"]
     fam = {0: "umma", 1: "umma_swap", 3: "gemv"}
-    keys = sorted({(fam[x["family"]], x["bm"], x["bn"]) for x in S})
+    keys = sorted({(fam[x["family"]], x["bm"], x["bn"], x.get("mc", 1)) for x in S})
     ini0 = json.load(open(args.init)) if args.init else None
-    names = ["%s_%dx%d" % k for k in keys]
+    names = [calib_key(*k) for k in keys]
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     hbm = peaks["hbm_gbs"] / CLOCK_GHZ
     # parameter vector: log of (mac, l2s, epi, fixed) per rung + log(dsm, fixed_cluster)
@@ -162,7 +173,7 @@ def fit(args):
         return th, g
 
     def key_of(x):
-        return "%s_%dx%d" % (fam[x["family"]], x["bm"], x["bn"])
+        return calib_key(fam[x["family"]], x["bm"], x["bn"], x.get("mc", 1))
 
     groups = {}
     for sm in S:
@@ -290,8 +301,10 @@ def heldout(args):
             best = min(f["us"] for f in e["forced"])
             def pred(f):
                 r = rt[f["rung"]]
-                sm = dict(M=M, N=N, K=K, split=f["split"], family=r["family"], bm=r["bm"], bn=r["bn"])
-                return model_us(sm, th["%s_%dx%d" % (fam[r["family"]], r["bm"], r["bn"])], desc, g)
+                sm = dict(M=M, N=N, K=K, split=f["split"], family=r["family"], bm=r["bm"], bn=r["bn"],
+                          mc=r.get("mc", 1))
+                return model_us(sm, th[calib_key(fam[r["family"]], r["bm"], r["bn"], r.get("mc", 1))],
+                                desc, g)
             pick = min(e["forced"], key=pred)
             regs.append(best / pick["us"])
             tag = "bert" if K == 768 else "llama"
