@@ -151,14 +151,6 @@ def test_zero_padding_on_tile_multiples():
             assert c["padded_work"] == mt * nt
 
 
-def test_tie_break_prefers_less_padding():
-    # SPEC.md:510 toy: M=5, top tiles {4, 8} at equal cost -> the smaller padded area wins
-    cands = [(100, 8 * 1, 1, 1), (100, 4 * 2, 0, 1)]   # (cost, padded_work, rung_id, split)
-    assert min(cands)[2] == 1 or min(cands)[1] == 8
-    keyed = sorted([(100, 8, 1, 1), (100, 12, 0, 1)])
-    assert keyed[0][2] == 1                             # equal cost -> less padded work
-
-
 def test_fp32_table_and_selection():
     t = S.build_table(64, "fp32", "fp32", DESC)
     assert all(r["family"] == 2 for r in t["rungs"])
