@@ -135,11 +135,11 @@ CLUSTER_MAX = 8                                  # portable cluster size
 
 # kernels that exist in the library (the "implemented" filter, R6):
 #   family 0: tcgen05, A-tile on the UMMA-M axis: cta_group::1 BM=128, BN in {64,128,192,256};
-#             cta_group::2 pairs BM=256, BN in {128,256}
+#             cta_group::2 pairs BM=256, BN in {64 (B stored N x K only),128,256}
 #   family 1: same kernel with A/B swapped (N on UMMA-M, M on UMMA-N; BN in
 #             {16,32,64,128,192,256})
 #   family 2: fp32 SIMT FFMA (BM, BN, TM, TN) in {(32,32,2,4),(64,64,4,4),(128,64,8,4)}
-IMPL_TC = {(0, 128, 64), (0, 128, 128), (0, 128, 192), (0, 128, 256), (0, 256, 128),
+IMPL_TC = {(0, 128, 64), (0, 128, 128), (0, 128, 192), (0, 128, 256), (0, 256, 64), (0, 256, 128),
            (0, 256, 256), (1, 128, 16), (1, 128, 32), (1, 128, 64), (1, 128, 128),
            (1, 128, 192), (1, 128, 256)}
 # TMA-multicast cluster kernels: (family, bm, bn, mc), mc CTAs sharing the A tile
@@ -210,6 +210,10 @@ def build_table(K: int, in_dtype: str, out_dtype: str, desc: dict, b_layout: str
             cg = 2 if bm == 256 else 1
             for swap in (0, 1):
                 if cg == 2 and swap:      # cta_group::2 pair rungs are non-swapped
+                    continue
+                # a pair CTA with < 64 B rows needs K-major B: the MN-major 128-B swizzle
+                # atom (B stored K x N) is 64 elements wide
+                if cg == 2 and bn // 2 < 64 and b_layout != "nk":
                     continue
                 stage_bytes = (bm // cg + bn // cg) * bk * in_b
                 for mc in MC_SIZES:

@@ -33,6 +33,7 @@ static const RungCalib kRungs[] = {
     {"umma_128x128", 1442773, 145125, 16764, 1203},
     {"umma_128x256", 1672861, 84000, 512000, 500},
     {"umma_256x128", 3297280, 160000, 33559, 5273},
+    {"umma_256x64", 3297280, 160000, 33559, 5273},   // provisional (= 256x128)
     {"umma_256x256", 4096000, 152381, 72112, 500},
     {"umma_swap_128x16", 1000000, 20745, 8000, 4053},
     {"umma_swap_128x32", 1000000, 28993, 8000, 4531},

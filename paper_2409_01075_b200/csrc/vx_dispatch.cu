@@ -42,7 +42,7 @@ bool kernel_available(int family, int bm, int bn, int mc) {
     if (mc != 1) return mc_available(family, bm, bn, mc);
     if (family == kUmma)
         return (bm == 128 && (bn == 64 || bn == 128 || bn == 192 || bn == 256)) ||
-               (bm == 256 && (bn == 128 || bn == 256));     // cta_group::2 pair rungs
+               (bm == 256 && (bn == 64 || bn == 128 || bn == 256));   // cta_group::2 pairs
     if (family == kUmmaSwap)
         return bm == 128 && (bn == 16 || bn == 32 || bn == 64 || bn == 128 || bn == 192 || bn == 256);
     if (family == kSimt) return (bm == 32 && bn == 32) || (bm == 64 && bn == 64) || (bm == 128 && bn == 64);
@@ -85,6 +85,9 @@ static UmmaFn umma_fn(int family, int bm, int bn, bool b_mn, int mc = 1) {
     }
     if (family == kUmma && bm == 256) {
         switch (bn) {
+        case 64:   // each CTA holds 32 B rows: K-major B only (an MN-major 128-B swizzle
+                   // atom is 64 elements wide), vx_plan keeps this rung for VX_B_NK only
+            return b_mn ? nullptr : (UmmaFn)vx_umma_kernel<64, false, false, false, true>;
         case 128: return pick_pair<128>(b_mn);
         case 256: return pick_pair<256>(b_mn);
         }

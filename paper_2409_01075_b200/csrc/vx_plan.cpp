@@ -136,6 +136,9 @@ static vx_status build_rungs(vx_plan_s* p) {
             for (int swap = 0; swap <= 1; ++swap) {
                 int fam = swap ? kUmmaSwap : kUmma;
                 if (cg == 2 && swap) continue;      // pair rungs are non-swapped
+                // a pair CTA holding fewer than 64 B rows needs B K-major (VX_B_NK): the
+                // MN-major 128-B swizzle atom (B stored K x N) is 64 elements wide
+                if (cg == 2 && c.bn / 2 < 64 && p->bl != VX_B_NK) continue;
                 int64_t stage = (int64_t)(c.bm / cg + c.bn / cg) * c.bk * in_b;
                 // TMA-multicast clusters of mc CTAs sharing the A tile: the
                 // multicast sub-box (A rows / mc) must be whole 8-row swizzle atoms and a

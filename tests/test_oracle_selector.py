@@ -181,7 +181,7 @@ def test_streamk_only_for_few_waves():
         if ch["split"] == 0:
             r = t["rungs"][ch["rung_id"]]
             assert S.streamk_admissible(r, 1, M, 11008, 4096, DESC)
-    big = [r for r in t["rungs"] if r["cg"] == 2 and r["family"] == 0][0]
+    big = [r for r in t["rungs"] if r["cg"] == 2 and r["family"] == 0 and r["bn"] == 256][0]
     assert not S.streamk_admissible(big, 1, 16384, 11008, 4096, DESC)
     assert S.streamk_admissible(big, 1, 512, 11008, 4096, DESC)
     # few k-blocks per CTA (BERT-size K, many small tiles): a tile would be cut over > 3 CTAs
