@@ -184,6 +184,23 @@ vx_status vx_gemm_ex(vx_plan_t plan, int64_t batch, int64_t M, int64_t N, int64_
                      const void* A, int64_t sA, const void* B, int64_t sB, void* C, int64_t sC,
                      int32_t force_rung, int32_t force_split, void* stream, vx_choice* used);
 
+/* Fused GEMM + row all-gather (BASELINE.json configs[4] "optional NCCL
+ * all-gather of C", PAPER.md:866-867 row independence): computes this rank's C_local =
+ * A x B (M rows, batch 1) and writes it -- tile by tile, straight from the GEMM epilogue, so
+ * the transfer of finished tiles overlaps the mainloop of later ones -- into rows
+ * [row_offset, row_offset + M) of EVERY destination dst[0..ndst), 1 <= ndst <= 8.  Each
+ * destination is a row-major [*, N] matrix of the plan's output dtype with at least
+ * row_offset + M rows: typically every rank's gathered C, mapped into this process (NVLink
+ * peer or symmetric-memory pointers, paper_2409_01075_b200/dist.py), this rank's own
+ * included.  No C is written besides the destinations.  Candidates are the non-swapped
+ * tcgen05 rungs with split 1 or stream-K (force_rung < 0 selects among them with the cost
+ * model; a forced pair outside that set is VX_ERR_INVALID).  Synchronisation with the
+ * readers (e.g. a barrier after the stream completes) is the caller's.  `used` (optional)
+ * receives the launched decision. */
+vx_status vx_gemm_gather(vx_plan_t plan, int64_t M, int64_t N, int64_t K, const void* A,
+                         const void* B, int32_t ndst, void* const* dst, int64_t row_offset,
+                         int32_t force_rung, int32_t force_split, void* stream, vx_choice* used);
+
 /* Host-staged form (the e2e measurement): A, B, C are HOST pointers (pinned for full
  * speed); dA, dB, dC are caller-owned device buffers of the same sizes.  Enqueues
  * H2D(A,B) -> vx_gemm_batched -> D2H(C) on `stream` and returns without synchronising. */

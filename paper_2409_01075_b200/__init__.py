@@ -94,6 +94,8 @@ def _load():
     L.vx_gemm_ex.argtypes = [P, i64, i64, i64, i64, vp, i64, vp, i64, vp, i64, i32, i32, vp,
                              ctypes.POINTER(Choice)]
     L.vx_gemm_host.argtypes = [P, i64, i64, i64, i64, vp, vp, vp, vp, vp, vp, vp]
+    L.vx_gemm_gather.argtypes = [P, i64, i64, i64, vp, vp, i32, ctypes.POINTER(vp), i64, i32,
+                                 i32, vp, ctypes.POINTER(Choice)]
     L.vx_launch_count.restype = i64
     L.vx_packed_b_elems.restype = i64
     L.vx_packed_b_elems.argtypes = [P, i64, i64, i64]
@@ -101,7 +103,7 @@ def _load():
     L.vx_pack_b.restype = ctypes.c_int
     for f in ("vx_device_probe", "vx_plan", "vx_plan_ex", "vx_plan_destroy", "vx_plan_select",
               "vx_plan_cost", "vx_plan_dump", "vx_gemm", "vx_gemm_batched", "vx_gemm_ex",
-              "vx_gemm_host"):
+              "vx_gemm_host", "vx_gemm_gather"):
         getattr(L, f).restype = ctypes.c_int
     if L.vx_abi_version() != 1:
         raise ImportError("libvx.so ABI %d != binding ABI 1 (rebuild)" % L.vx_abi_version())
@@ -254,6 +256,33 @@ class Plan:
         """Raw-pointer form (bench hot loop): no tensor checks, same C call."""
         _check(_lib.vx_gemm_batched(self._h, batch, M, N, K, A, sA, B, sB, C, sC, stream_ptr),
                "vx_gemm_batched")
+
+    def gemm_gather(self, A, B, dsts, row_offset: int, stream=None,
+                    force: tuple[int, int] | None = None, want_choice: bool = False):
+        """Fused GEMM + row all-gather (vx_gemm_gather): C_local = A x B written into rows
+        [row_offset, row_offset + M) of every destination.  dsts: CUDA tensors (same device
+        as A) or raw device pointers (e.g. symmetric-memory peer buffers)."""
+        M, K = A.shape
+        N = self.N
+        for t, nm in ((A, "A"), (B, "B")):
+            if not t.is_cuda or not t.is_contiguous() or _dt_name(t) != self.in_dtype:
+                raise ValueError("%s must be a contiguous CUDA %s tensor" % (nm, self.in_dtype))
+        ptrs = []
+        for d in dsts:
+            if isinstance(d, int):
+                ptrs.append(d)
+                continue
+            if not d.is_cuda or not d.is_contiguous() or d.shape[-1] != N or d.shape[0] < row_offset + M:
+                raise ValueError("gather destination must be a contiguous CUDA [>= %d, %d] tensor"
+                                 % (row_offset + M, N))
+            ptrs.append(d.data_ptr())
+        arr = (ctypes.c_void_p * len(ptrs))(*ptrs)
+        ch = Choice()
+        fr, fs = force if force is not None else (-1, 0)
+        _check(_lib.vx_gemm_gather(self._h, M, N, K, A.data_ptr(), B.data_ptr(), len(ptrs), arr,
+                                   row_offset, fr, fs, _stream_ptr(stream), ctypes.byref(ch)),
+               "vx_gemm_gather")
+        return ch.as_dict() if want_choice else None
 
     def gemm_host(self, batch, M, N, K, hA, hB, hC, dA, dB, dC, stream_ptr):
         _check(_lib.vx_gemm_host(self._h, batch, M, N, K, hA, hB, hC, dA, dB, dC, stream_ptr),

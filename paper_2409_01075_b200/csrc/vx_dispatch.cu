@@ -325,7 +325,7 @@ static vx_status ensure_ws(const vx_plan_s* pc, void* stream, void** out) {
 
 vx_status launch(const vx_plan_s* p, const vx_choice& ch, int64_t batch, int64_t M, int64_t N,
                  int64_t K, const void* A, int64_t sA, const void* B, int64_t sB, void* C,
-                 int64_t sC, void* stream) {
+                 int64_t sC, void* stream, const GatherSpec* gather) {
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     const vx::Rung& r = p->rungs[ch.rung_id];
     if (r.family == kSimt) {
@@ -469,6 +469,20 @@ vx_status launch(const vx_plan_s* p, const vx_choice& ch, int64_t batch, int64_t
     const int ob = p->out == VX_FP32 ? 4 : 2;
     prm.vec = (N % 8 == 0) && ((prm.sC * ob) % 16 == 0) &&
               ((reinterpret_cast<uintptr_t>(C) & 15) == 0);
+    prm.ndst = 0;
+    prm.dst_row0 = 0;
+    for (int d = 0; d < 8; ++d) prm.dst[d] = nullptr;
+    if (gather) {
+        // fused all-gather epilogue: vector stores iff every destination
+        // row is 16-B aligned
+        prm.ndst = gather->ndst;
+        prm.dst_row0 = gather->row0;
+        prm.vec = N % 8 == 0;
+        for (int d = 0; d < gather->ndst; ++d) {
+            prm.dst[d] = gather->dst[d];
+            if (reinterpret_cast<uintptr_t>(gather->dst[d]) & 15) prm.vec = 0;
+        }
+    }
     // C map for the TMA-store epilogue: non-swap boxes are 128-B rows x 32 rows (swizzled),
     // swap boxes are 32 n x min(32, BN) m (plain)
     CUtensorMap mapC;
@@ -656,6 +670,38 @@ vx_status vx_gemm_batched(vx_plan_t p, int64_t batch, int64_t M, int64_t N, int6
 vx_status vx_gemm(vx_plan_t p, int64_t M, int64_t N, int64_t K, const void* A, const void* B,
                   void* C, void* stream) {
     return vx_gemm_ex(p, 1, M, N, K, A, M * K, B, N * K, C, M * N, -1, 0, stream, nullptr);
+}
+
+vx_status vx_gemm_gather(vx_plan_t p, int64_t M, int64_t N, int64_t K, const void* A,
+                         const void* B, int32_t ndst, void* const* dst, int64_t row_offset,
+                         int32_t force_rung, int32_t force_split, void* stream, vx_choice* used) {
+    if (!p || !dst || ndst < 1 || ndst > 8 || row_offset < 0) {
+        set_error("gather needs 1 <= ndst <= 8 destinations and row_offset >= 0");
+        return VX_ERR_INVALID;
+    }
+    for (int d = 0; d < ndst; ++d)
+        if (!dst[d]) { set_error("NULL gather destination %d", d); return VX_ERR_INVALID; }
+    if (p->in == VX_FP32) { set_error("gather needs 16-bit inputs (tcgen05 rungs)"); return VX_ERR_UNSUPPORTED; }
+    vx_status s = check_args(p, 1, M, N, K, A, M * K, B, N * K, dst[0], M * N);
+    if (s != VX_OK) return s;
+    if (M == 0) return VX_OK;
+    if (p->device >= 0) {
+        int cur = -1;
+        if (cudaGetDevice(&cur) != cudaSuccess || cur != p->device) {
+            cudaGetLastError();
+            set_error("current device %d != the plan's device %d", cur, p->device);
+            return VX_ERR_INVALID;
+        }
+    }
+    vx_choice ch;
+    s = select_choice(p, 1, M, N, force_rung, force_split, &ch, kSelectGather);
+    if (s != VX_OK) return s;
+    if (used) *used = ch;
+    GatherSpec g;
+    g.ndst = ndst;
+    g.row0 = row_offset;
+    for (int d = 0; d < 8; ++d) g.dst[d] = d < ndst ? dst[d] : nullptr;
+    return launch(p, ch, 1, M, N, K, A, M * K, B, N * K, dst[0], M * N, stream, &g);
 }
 
 vx_status vx_gemm_host(vx_plan_t p, int64_t batch, int64_t M, int64_t N, int64_t K,

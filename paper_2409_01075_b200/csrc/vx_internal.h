@@ -88,15 +88,27 @@ struct vx_plan_s {
 };
 
 namespace vx {
+// fused GEMM + row all-gather destinations (vx_gemm_gather)
+struct GatherSpec {
+    int32_t ndst;
+    void* dst[8];
+    int64_t row0;
+};
+// candidate filters of the runtime selection
+enum SelectFilter : int32_t {
+    kSelectAll = 0,
+    kSelectGather = 1,   // rungs whose epilogue can fan out rows: non-swapped tcgen05, split 1 / 0
+};
 // vx_plan.cpp
 vx_status select_choice(const vx_plan_s* p, int64_t batch, int64_t M, int64_t N,
-                        int32_t force_rung, int32_t force_split, vx_choice* out);
+                        int32_t force_rung, int32_t force_split, vx_choice* out,
+                        int32_t filter = kSelectAll);
 int in_bytes(vx_dtype d);
 int out_bytes(vx_dtype d);
 void set_error(const char* fmt, ...);
 // vx_dispatch.cu
 vx_status launch(const vx_plan_s* p, const vx_choice& ch, int64_t batch, int64_t M, int64_t N,
                  int64_t K, const void* A, int64_t sA, const void* B, int64_t sB, void* C,
-                 int64_t sC, void* stream);
+                 int64_t sC, void* stream, const GatherSpec* gather = nullptr);
 vx_status prepare_kernels(const vx_plan_s* p);
 }  // namespace vx

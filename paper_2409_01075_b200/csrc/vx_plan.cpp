@@ -362,8 +362,14 @@ static inline int64_t padded_work(const vx_choice& c, int64_t batch) {
     return batch * tm * c.bm * tn * c.bn;
 }
 
+static bool passes(int32_t filter, const Rung& r, int s) {
+    if (filter == kSelectGather) return r.family == kUmma && (s == 0 || s == 1);
+    return true;
+}
+
 vx_status select_choice(const vx_plan_s* p, int64_t batch, int64_t M, int64_t N,
-                        int32_t force_rung, int32_t force_split, vx_choice* out) {
+                        int32_t force_rung, int32_t force_split, vx_choice* out,
+                        int32_t filter) {
     if (!p || !out) { set_error("NULL argument"); return VX_ERR_INVALID; }
     if (batch < 1 || M < 1 || N < 1) { set_error("batch, M, N must be >= 1"); return VX_ERR_INVALID; }
     if (p->N > 0 && N != p->N) { set_error("N=%lld does not match the plan's N=%lld", (long long)N, (long long)p->N); return VX_ERR_INVALID; }
@@ -378,10 +384,15 @@ vx_status select_choice(const vx_plan_s* p, int64_t batch, int64_t M, int64_t N,
             set_error("GEMV rung %d holds at most %d rows", force_rung, r.bm);
             return VX_ERR_INVALID;
         }
+        if (!passes(filter, r, force_split)) {
+            set_error("rung %d split %d cannot fan out rows (gather needs a non-swapped tcgen05 "
+                      "rung with split 1 or 0)", force_rung, force_split);
+            return VX_ERR_INVALID;
+        }
         rung_cost(p, r, force_split, batch, M, N, out);
         return VX_OK;
     }
-    const bool memo = batch == 1 && p->N > 0 && M <= vx_plan_s::kMemo;
+    const bool memo = batch == 1 && p->N > 0 && M <= vx_plan_s::kMemo && filter == kSelectAll;
     if (memo && p->memo_state[M].load(std::memory_order_acquire) == 2) {
         *out = p->memo[M];
         return VX_OK;
@@ -393,6 +404,7 @@ vx_status select_choice(const vx_plan_s* p, int64_t batch, int64_t M, int64_t N,
         for (int s : r.splits) {
             if (s == 0 && !sk_admissible(p, r, batch, M, N)) continue;
             if (r.family == kGemv && M > r.bm) continue;   // GEMV rungs hold M <= MT rows
+            if (!passes(filter, r, s)) continue;
             vx_choice c;
             rung_cost(p, r, s, batch, M, N, &c);
             if (!have || std::make_tuple(c.cost, padded_work(c, batch), c.rung_id, c.split) <

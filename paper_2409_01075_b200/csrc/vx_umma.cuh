@@ -69,6 +69,12 @@ struct UmmaParams {
     int mc;                     // TMA-multicast cluster size (1 = none): MC CTAs share the A
                                 // operand tile (P when non-swapped, Q when swapped); tiles
                                 // and num_tiles then count cluster tiles
+    int ndst;                   // fused GEMM + row all-gather: > 0 = the
+                                // epilogue writes every finished C row chunk straight from
+                                // registers into rows dst_row0 + m of each dst[d] (peer /
+                                // symmetric-memory buffers over NVLink); C is not written
+    long long dst_row0;
+    void* dst[8];
     int kdouble;                // 1: two-chunk loads (tmP2 / tmQ2) fill two adjacent ring
                                 // stages with one TMA box per operand (K % 64 == 0, K-major
                                 // P and Q, unpacked; rings of >= 6 stages, >= 8 for pair
@@ -806,7 +812,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 continue;
             }
-            if (p.vec && !(p.dbg & 8)) {
+            if (p.vec && p.ndst == 0 && !(p.dbg & 8)) {
                 // TMEM -> registers -> swizzled SMEM staging -> TMA bulk store (full lines,
                 // asynchronous, M/N tails clipped by the tensor map)
                 const int ob = p.out_kind == 2 ? 4 : 2;
@@ -914,10 +920,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                 } else if (!SWAP) {
                     // row pr = m, columns = n
                     if (pr < p.M) {
-                        const long long base = (long long)pr * p.ldc;
                         const int n0 = tq * BN + c * 32;
-                        if (p.vec) store_row_chunk<W>(Cb, base, n0, p.N, f, p.out_kind);
-                        else store_row_scalar(Cb, base, n0, p.N, W, f, p.out_kind);
+                        if (p.ndst > 0) {
+                            // fused all-gather: the same chunk into every destination, at
+                            // its global row (peer stores travel over NVLink while the
+                            // next tile's mainloop runs, TMEM being double-buffered)
+                            const long long base = (p.dst_row0 + pr) * p.ldc;
+#pragma unroll 1
+                            for (int d = 0; d < p.ndst; ++d) {
+                                char* Db = reinterpret_cast<char*>(p.dst[d]);
+                                if (p.vec) store_row_chunk<W>(Db, base, n0, p.N, f, p.out_kind);
+                                else store_row_scalar(Db, base, n0, p.N, W, f, p.out_kind);
+                            }
+                        } else {
+                            const long long base = (long long)pr * p.ldc;
+                            if (p.vec) store_row_chunk<W>(Cb, base, n0, p.N, f, p.out_kind);
+                            else store_row_scalar(Cb, base, n0, p.N, W, f, p.out_kind);
+                        }
                     }
                 } else if (pr < p.N) {
                     // row pr = n, columns = m

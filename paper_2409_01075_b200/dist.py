@@ -6,6 +6,13 @@ and no reduction is needed.  A gathered C is produced only when asked for, with 
 collective: all_gather_into_tensor over NCCL (NVLink 5 / NVSwitch on B200).  Uneven M is
 handled by padding every shard to the largest shard in the gather buffer and trimming.
 
+Fused variant: instead of GEMM then all_gather, every rank's GEMM
+epilogue writes its finished C tiles straight into the gathered C of EVERY rank
+(vx_gemm_gather), over NVLink through symmetric-memory peer pointers
+(torch.distributed._symmetric_memory), so the transfer overlaps the mainloop of later
+tiles; one barrier then orders the readers.  gather_plan() computes the pure host-side part
+(row offsets and the destination order), which the gloo tests check on CPU.
+
 Everything here is host-side plumbing; the GEMM itself is the library call.  The
 collective goes through a torch.distributed process group, so the same code runs on the
 "gloo" backend with CPU tensors (tests/test_dist.py) and on "nccl" with CUDA tensors.
@@ -53,6 +60,82 @@ def gather_rows(c_local: torch.Tensor, M: int, group=None) -> torch.Tensor:
         return recv
     parts = [recv[r * mmax: r * mmax + sizes[r]] for r in range(world)]
     return torch.cat(parts, 0)
+
+
+def gather_plan(M: int, world: int, rank: int) -> dict:
+    """Host-side plan of the fused GEMM + all-gather for one rank: the rows it computes, the
+    row offset its epilogue writes at in every destination, and the destination order
+    (its own buffer first, then the peers in rank order)."""
+    lo, hi = row_shard(M, world, rank)
+    return {"rows": (lo, hi), "row_offset": lo,
+            "dst_ranks": [rank] + [r for r in range(world) if r != rank]}
+
+
+def push_rows(c_local: torch.Tensor, M: int, group=None) -> torch.Tensor:
+    """The fused gather's data movement with point-to-point sends instead of peer stores
+    (any backend, e.g. gloo on CPU): every rank pushes its C rows to every destination in
+    gather_plan order, and each destination places the rows of rank r at row_offset(r) --
+    the placement rule the vx_gemm_gather epilogue applies on NVLink."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    gp = gather_plan(M, world, rank)
+    lo, hi = gp["rows"]
+    if c_local.shape[0] != hi - lo:
+        raise ValueError("local shard has %d rows, expected %d" % (c_local.shape[0], hi - lo))
+    out = torch.empty((M, c_local.shape[1]), dtype=c_local.dtype, device=c_local.device)
+    out[lo:hi] = c_local
+    reqs = []
+    for dst in gp["dst_ranks"][1:]:
+        reqs.append(dist.isend(c_local.contiguous(), dst, group=group))
+    for src in range(world):
+        if src == rank:
+            continue
+        slo, shi = gather_plan(M, world, src)["rows"]
+        if shi > slo:
+            buf = torch.empty((shi - slo, c_local.shape[1]), dtype=c_local.dtype,
+                              device=c_local.device)
+            dist.recv(buf, src, group=group)
+            out[slo:shi] = buf
+        else:
+            dist.recv(torch.empty((0, c_local.shape[1]), dtype=c_local.dtype), src, group=group)
+    for r in reqs:
+        r.wait()
+    return out
+
+
+def symmetric_gather_buffer(M: int, N: int, dtype, device, group=None):
+    """Gathered C [M, N] in symmetric memory on every rank of `group`: returns (this rank's
+    tensor, handle, device pointers of every rank's buffer valid in this process)."""
+    import torch.distributed as dist
+    import torch.distributed._symmetric_memory as symm_mem
+    buf = symm_mem.empty((M, N), dtype=dtype, device=device)
+    hdl = symm_mem.rendezvous(buf, group if group is not None else dist.group.WORLD)
+    return buf, hdl, list(hdl.buffer_ptrs)
+
+
+def fused_gather_gemm(plan, A_shard: torch.Tensor, B: torch.Tensor, M: int, group=None,
+                      buf=None, stream=None):
+    """C = A x B row-sharded, gathered on every rank by the GEMM epilogue itself (no
+    separate collective).  A_shard: this rank's rows (row_shard).  Returns the gathered
+    [M, N] C (a symmetric-memory tensor).  `buf` = a (tensor, handle, ptrs) triple from
+    symmetric_gather_buffer to reuse."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    gp = gather_plan(M, world, rank)
+    lo, hi = gp["rows"]
+    if A_shard.shape[0] != hi - lo:
+        raise ValueError("A shard has %d rows, expected %d" % (A_shard.shape[0], hi - lo))
+    odt = {"bf16": torch.bfloat16, "fp16": torch.float16, "fp32": torch.float32}[plan.out_dtype]
+    if buf is None:
+        buf = symmetric_gather_buffer(M, plan.N, odt, A_shard.device, group)
+    out, hdl, ptrs = buf
+    hdl.barrier()               # every destination is allocated and free to be written
+    plan.gemm_gather(A_shard, B, [ptrs[r] for r in gp["dst_ranks"]], gp["row_offset"],
+                     stream=stream)
+    hdl.barrier()               # every rank's epilogue has written its rows everywhere
+    return out
 
 
 class ShardedGemm:

@@ -13,7 +13,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2409_01075_b200.dist import ShardedGemm, gather_rows, row_shard, shard_sizes
+from paper_2409_01075_b200.dist import (ShardedGemm, gather_plan, gather_rows, push_rows,
+                                        row_shard, shard_sizes)
 
 
 def test_row_shard_partition_properties():
@@ -57,7 +58,8 @@ def _worker(rank, world, port, M, N, K, q):
         C = sg.forward(A, B, gather=True)                # gathered on every rank
         lo_ = torch.tensor([lo], dtype=torch.int64)
         C2 = gather_rows(c_rows, M)                      # the gather alone
-        q.put((rank, ok_rows, C.numpy(), C2.numpy(), int(lo_)))
+        C3 = push_rows(c_rows, M)                        # the fused gather's push placement
+        q.put((rank, ok_rows, C.numpy(), C2.numpy(), int(lo_), C3.numpy()))
     finally:
         dist.destroy_process_group()
 
@@ -79,6 +81,24 @@ def test_sharded_gather_equals_full_gemm(world, M):
         assert p.exitcode == 0
     A, B = synth.gemm_inputs(M, N, K, "fp32", "nk", kind="int", seed=42)
     want = oracle.gemm(A, B, "nk")
-    for rank, ok_rows, C, C2, lo in res:
+    for rank, ok_rows, C, C2, lo, C3 in res:
         assert ok_rows
         assert np.array_equal(C, want) and np.array_equal(C2, want)
+        assert np.array_equal(C3, want)
+
+
+def test_gather_plan_covers_every_destination_once():
+    """Fused GEMM + all-gather: each rank's epilogue writes its rows at its
+    row_shard offset into every rank's buffer, its own first; over all ranks every
+    (destination, row) is written exactly once."""
+    for M in (1, 37, 1000, 65536):
+        for world in (1, 2, 3, 8):
+            hits = np.zeros((world, M), dtype=np.int64)
+            for r in range(world):
+                gp = gather_plan(M, world, r)
+                lo, hi = gp["rows"]
+                assert gp["row_offset"] == lo and gp["dst_ranks"][0] == r
+                assert sorted(gp["dst_ranks"]) == list(range(world))
+                for d in gp["dst_ranks"]:
+                    hits[d, lo:hi] += 1
+            assert (hits == 1).all()

@@ -464,3 +464,69 @@ def test_batched_gemm_rejects_unbatched_b():
         p.gemm(Q, torch.zeros((16, 64), dtype=torch.bfloat16, device="cuda"))
     with pytest.raises(ValueError):
         p.gemm(Q, torch.zeros((3, 16, 64), dtype=torch.bfloat16, device="cuda"))
+
+
+@pytest.mark.parametrize("bl", ["nk", "kn"])
+def test_fused_gemm_gather_integer_exact(bl):
+    """vx_gemm_gather on one GPU: three simulated ranks each compute their
+    row shard and their epilogues write it into all three gathered buffers; every buffer
+    must equal the full product bit for bit, for every gather-capable (rung, split) -- the
+    non-swapped tcgen05 rungs, persistent / pair / multicast / stream-K -- with ragged
+    shards (M = 333 -> 111 rows each, partial tiles) and untouched rows past M."""
+    from paper_2409_01075_b200.dist import gather_plan
+    vx = vxmod()
+    M, N, K = 333, 384, 512
+    world = 3
+    p = vx.Plan(N, K, "bf16", "fp32", bl)
+    A, B = synth.gemm_inputs(M, N, K, "bf16", bl, kind="int", seed=77)
+    want = oracle.gemm(A, B, bl)
+    Ad, Bd = A.cuda(), B.cuda()
+    cands = [(r["rung_id"], s) for r in p.dump()["rungs"] if r["family"] == 0
+             for s in r["splits"] if s in (0, 1)]
+    assert any(r["cg"] == 2 for r in p.dump()["rungs"] if r["family"] == 0)
+    for force in cands + [None]:
+        bufs = [torch.full((M + 16, N), 7.0, dtype=torch.float32, device="cuda")
+                for _ in range(world)]
+        for r in range(world):
+            gp = gather_plan(M, world, r)
+            lo, hi = gp["rows"]
+            ch = p.gemm_gather(Ad[lo:hi].contiguous(), Bd, [bufs[d] for d in gp["dst_ranks"]],
+                               gp["row_offset"], force=force, want_choice=True)
+            assert ch["family"] == 0 and ch["split"] in (0, 1)
+        torch.cuda.synchronize()
+        for b in bufs:
+            got = b.cpu().double().numpy()
+            assert np.array_equal(got[:M], want), (bl, force)
+            assert np.all(got[M:] == 7.0)
+    with pytest.raises(vx.VxError):       # a swapped rung cannot fan out rows
+        sw = [r["rung_id"] for r in p.dump()["rungs"] if r["family"] == 1][0]
+        p.gemm_gather(Ad, Bd, [bufs[0]], 0, force=(sw, 1))
+
+
+def test_fused_gemm_gather_symmetric_memory_single_rank():
+    """dist.fused_gather_gemm through torch symmetric memory on a 1-rank NCCL group (the
+    multi-rank run maps peer buffers the same way; it stays unmeasured on one GPU)."""
+    import os
+    import socket
+    import torch.distributed as dist
+    from paper_2409_01075_b200.dist import fused_gather_gemm
+    vx = vxmod()
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        M, N, K = 300, 512, 256
+        A, B = synth.gemm_inputs(M, N, K, "bf16", "nk", kind="int", seed=5)
+        p = vx.Plan(N, K, "bf16", "fp32", "nk")
+        try:
+            C = fused_gather_gemm(p, A.cuda(), B.cuda(), M)
+        except (RuntimeError, NotImplementedError) as e:   # no symmetric-memory backend
+            pytest.skip("symmetric memory unavailable: %s" % e)
+        torch.cuda.synchronize()
+        assert np.array_equal(C.cpu().double().numpy(), oracle.gemm(A, B, "nk"))
+    finally:
+        dist.destroy_process_group()
