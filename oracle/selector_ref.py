@@ -279,13 +279,16 @@ def build_table(K: int, in_dtype: str, out_dtype: str, desc: dict, b_layout: str
 # Runtime cost and selection ("vx_plan_select")
 # ----------------------------------------------------------------------------------------
 
-def _calib_for(rung: dict, calib: dict) -> dict:
+def _calib_key(rung: dict) -> str:
+    """Calibration-table key of a rung: family, TMA-multicast cluster size, tile."""
     fam = FAMILY_NAMES[rung["family"]]
     if rung.get("mc", 1) > 1:
-        key = "%s_mc%d_%dx%d" % (fam, rung["mc"], rung["bm"], rung["bn"])
-    else:
-        key = "%s_%dx%d" % (fam, rung["bm"], rung["bn"])
-    return calib["rungs"][key]
+        return "%s_mc%d_%dx%d" % (fam, rung["mc"], rung["bm"], rung["bn"])
+    return "%s_%dx%d" % (fam, rung["bm"], rung["bn"])
+
+
+def _calib_for(rung: dict, calib: dict) -> dict:
+    return calib["rungs"][_calib_key(rung)]
 
 
 def simt_slots(rung: dict, desc: dict) -> int:

@@ -22,37 +22,37 @@
 namespace vx {
 
 static const Calib kCalib = {
-    /*hbm_milli=*/3335674,   // 6543 GB/s measured copy bandwidth / 1.965 GHz
+    /*hbm_milli=*/3327023,   // 6543 GB/s measured copy bandwidth / 1.965 GHz
     /*dsm_milli=*/2931,      // effective in-cluster reduce rate (fitted)
-    /*fixed_cluster=*/206,  // cluster launch + two cluster barriers (fitted)
-    /*skfix_milli=*/19022,   // stream-K partial write + read-back (fitted)
+    /*fixed_cluster=*/1051,  // cluster launch + two cluster barriers (fitted)
+    /*skfix_milli=*/13315,   // stream-K partial write + read-back (fitted)
 };
 
 static const RungCalib kRungs[] = {
-    {"umma_128x64", 1000367, 44315, 8000, 7631},
-    {"umma_128x128", 1442773, 145125, 16764, 1203},
-    {"umma_128x256", 1672861, 84000, 512000, 500},
-    {"umma_256x128", 3297280, 160000, 33559, 5273},
-    {"umma_256x64", 3297280, 160000, 33559, 5273},   // provisional (= 256x128)
-    {"umma_256x256", 4096000, 152381, 72112, 500},
-    {"umma_swap_128x16", 1000000, 20745, 8000, 4053},
-    {"umma_swap_128x32", 1000000, 28993, 8000, 4531},
-    {"umma_swap_128x64", 1000000, 42147, 512000, 5892},
-    {"umma_swap_128x128", 1449009, 160000, 8000, 726},
-    // BN = 192 / swapped BN = 192, 256 (tile-boundary cliffs, R6): provisional constants
-    {"umma_128x192", 1600000, 100000, 32000, 800},
-    {"umma_swap_128x192", 1600000, 100000, 32000, 800},
-    {"umma_swap_128x256", 1672861, 84000, 32000, 800},
-    // TMA-multicast clusters: provisional = the unicast rung's constants
-    {"umma_mc2_128x128", 1442773, 145125, 16764, 1203},
-    {"umma_mc2_128x256", 1672861, 84000, 512000, 500},
-    {"umma_swap_mc2_128x32", 1000000, 28993, 8000, 4531},
-    {"umma_swap_mc2_128x64", 1000000, 42147, 512000, 5892},
-    {"umma_swap_mc4_128x64", 1000000, 42147, 512000, 5892},
-    {"gemv_1x8", 4328, 63578, 16000, 2628},
-    {"gemv_2x8", 8000, 74202, 1000, 3062},
-    {"gemv_4x8", 8762, 64524, 1000, 2428},
-    {"gemv_8x8", 8832, 5888, 1217, 200},
+    {"umma_128x64", 1000367, 46603, 8000, 7014},
+    {"umma_128x128", 1679365, 54422, 17537, 1757},
+    {"umma_128x256", 1923790, 152381, 42657, 200},
+    {"umma_256x128", 3611307, 86550, 31800, 2883},
+    {"umma_256x64", 2323400, 160000, 33190, 10650},
+    {"umma_256x256", 4096000, 160000, 62692, 1072},
+    {"umma_swap_128x16", 1000000, 33673, 8000, 4053},
+    {"umma_swap_128x32", 1000000, 45735, 10090, 4110},
+    {"umma_swap_128x64", 1183082, 53507, 11773, 2864},
+    {"umma_swap_128x128", 1597532, 86907, 16000, 1009},
+    // BN = 192 / swapped BN = 192, 256 (tile-boundary cliffs, R6)
+    {"umma_128x192", 1470000, 160000, 32438, 200},
+    {"umma_swap_128x192", 1738143, 132300, 32255, 338},
+    {"umma_swap_128x256", 1844329, 160000, 23044, 200},
+    // TMA-multicast clusters
+    {"umma_mc2_128x128", 1744850, 41151, 17435, 2426},
+    {"umma_mc2_128x256", 4096000, 38348, 512000, 3025},
+    {"umma_swap_mc2_128x32", 1000000, 36759, 8762, 6343},
+    {"umma_swap_mc2_128x64", 1043084, 40140, 512000, 6776},
+    {"umma_swap_mc4_128x64", 1000000, 36408, 512000, 6776},
+    {"gemv_1x8", 11796, 9609, 1000, 3022},
+    {"gemv_2x8", 9088, 43894, 1000, 3376},
+    {"gemv_4x8", 9215, 64524, 1000, 2932},
+    {"gemv_8x8", 10665, 5341, 148392, 676},
     {"simt_32x32", 128000, 32000, 16000, 2000},
     {"simt_64x64", 128000, 32000, 16000, 2000},
     {"simt_128x64", 128000, 32000, 16000, 2000},

@@ -50,7 +50,7 @@ def test_calibration_copies_agree():
     assert d["calib"] == {k: CAL[k] for k in ("hbm_milli", "dsm_milli", "fixed_cluster",
                                               "skfix_milli")}
     for r in d["rungs"]:
-        key = "%s_%dx%d" % (S.FAMILY_NAMES[r["family"]], r["bm"], r["bn"])
+        key = S._calib_key(r)
         for f in ("mac_milli", "l2s_milli", "epi_milli", "fixed"):
             assert r[f] == CAL["rungs"][key][f], (key, f)
     d = vx.Plan(64, 64, "fp32", "fp32", "nk", desc=DESC).dump()
