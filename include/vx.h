@@ -60,6 +60,8 @@ extern "C" {
 #define VX_ABI_VERSION 1
 
 typedef struct vx_plan_s* vx_plan_t; /* opaque, immutable after vx_plan */
+typedef struct vx_calib_s* vx_calib_t; /* opaque calibration (empirical tier), immutable once
+                                          handed to a plan */
 
 typedef enum { VX_BF16 = 0, VX_FP16 = 1, VX_FP32 = 2 } vx_dtype;
 
@@ -151,6 +153,42 @@ vx_status vx_plan_ex(int64_t N, int64_t K, vx_dtype in, vx_dtype out, vx_blayout
                      const vx_device_desc* desc, vx_plan_t* plan);
 
 vx_status vx_plan_destroy(vx_plan_t plan);
+
+/* ---- the empirical tier of the hybrid analyzer (Sec. 5.2) ----------
+ * Every plan prices its rungs with per-rung constants (mac / l2s / epi rates in bytes or
+ * MACs per SM cycle x1000, fixed cycles) plus chip constants.  By default
+ * they are the compiled-in table, measured offline on a B200 (vx_calib.cpp).  These entry
+ * points let a caller measure them LIVE on its device and freeze them into plans. */
+
+/* Profile every 16-bit tcgen05 / CUDA-core rung and schedule on `device` over a fixed
+ * generic grid of shapes (never a workload shape), fit the per-rung constants of the same
+ * integer Eqs. 2-4 vx_plan_select evaluates, and return them with the compiled-in chip
+ * constants.  bl: layout of B the timings use (VX_B_KN or VX_B_NK).
+ * effort 0: 4 (N,K) x 7 M (seconds); 1: 7 (N,K) x 14 M.  Allocates ~768 MB of device
+ * memory for the duration of the call; synchronises the device.  Free with
+ * vx_calib_destroy. */
+vx_status vx_calibrate(int device, vx_blayout bl, int32_t effort, vx_calib_t* out);
+
+/* A calibration from explicit values (e.g. a JSON table): chip constants, then one
+ * vx_calib_set_rung per rung key ("umma_128x128", "umma_swap_mc2_128x64", "gemv_4x8", ...;
+ * the keys vx_plan_dump reports through its rung fields). */
+vx_status vx_calib_new(int64_t hbm_milli, int64_t dsm_milli, int64_t fixed_cluster,
+                       int64_t skfix_milli, vx_calib_t* out);
+vx_status vx_calib_set_rung(vx_calib_t calib, const char* key, int64_t mac_milli,
+                            int64_t l2s_milli, int64_t epi_milli, int64_t fixed);
+vx_status vx_calib_destroy(vx_calib_t calib);
+
+/* Canonical JSON of a calibration ({"source", chip constants, "rungs": {key: {...}}});
+ * calib NULL = the compiled-in table.  Same buffer protocol as vx_plan_dump. */
+vx_status vx_calib_dump(vx_calib_t calib, char* buf, size_t cap, size_t* need);
+
+/* vx_plan / vx_plan_ex with the given calibration (copied: the plan owns its copy, the
+ * calibration may be destroyed afterwards).  A rung whose key the calibration lacks makes
+ * the call fail with VX_ERR_UNSUPPORTED. */
+vx_status vx_plan_calibrated(int64_t N, int64_t K, vx_dtype in, vx_dtype out, vx_blayout bl,
+                             int device, vx_calib_t calib, vx_plan_t* plan);
+vx_status vx_plan_ex_calibrated(int64_t N, int64_t K, vx_dtype in, vx_dtype out, vx_blayout bl,
+                                const vx_device_desc* desc, vx_calib_t calib, vx_plan_t* plan);
 
 /* Runtime selection only (host, pure, deterministic): argmin of Eq. 4 cost over the
  * plan's (rung, split) pairs for (batch, M, N).  N must equal the plan's N when static

@@ -12,8 +12,8 @@ import ctypes
 import json
 import os
 
-__all__ = ["VxError", "Plan", "DeviceDesc", "Choice", "lib", "plan", "gemm", "gemm_batched",
-           "device_probe", "launch_count", "LIB_PATH"]
+__all__ = ["VxError", "Plan", "DeviceDesc", "Choice", "Calib", "lib", "plan", "gemm",
+           "gemm_batched", "device_probe", "launch_count", "calibrate", "LIB_PATH"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libvx.so")
 
@@ -96,6 +96,15 @@ def _load():
     L.vx_gemm_host.argtypes = [P, i64, i64, i64, i64, vp, vp, vp, vp, vp, vp, vp]
     L.vx_gemm_gather.argtypes = [P, i64, i64, i64, vp, vp, i32, ctypes.POINTER(vp), i64, i32,
                                  i32, vp, ctypes.POINTER(Choice)]
+    L.vx_calibrate.argtypes = [ctypes.c_int, ctypes.c_int, i32, ctypes.POINTER(P)]
+    L.vx_calib_new.argtypes = [i64, i64, i64, i64, ctypes.POINTER(P)]
+    L.vx_calib_set_rung.argtypes = [P, ctypes.c_char_p, i64, i64, i64, i64]
+    L.vx_calib_destroy.argtypes = [P]
+    L.vx_calib_dump.argtypes = [P, ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]
+    L.vx_plan_calibrated.argtypes = [i64, i64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                     ctypes.c_int, P, ctypes.POINTER(P)]
+    L.vx_plan_ex_calibrated.argtypes = [i64, i64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                        ctypes.POINTER(DeviceDesc), P, ctypes.POINTER(P)]
     L.vx_launch_count.restype = i64
     L.vx_packed_b_elems.restype = i64
     L.vx_packed_b_elems.argtypes = [P, i64, i64, i64]
@@ -103,7 +112,9 @@ def _load():
     L.vx_pack_b.restype = ctypes.c_int
     for f in ("vx_device_probe", "vx_plan", "vx_plan_ex", "vx_plan_destroy", "vx_plan_select",
               "vx_plan_cost", "vx_plan_dump", "vx_gemm", "vx_gemm_batched", "vx_gemm_ex",
-              "vx_gemm_host", "vx_gemm_gather"):
+              "vx_gemm_host", "vx_gemm_gather", "vx_calibrate", "vx_calib_new",
+              "vx_calib_set_rung", "vx_calib_destroy", "vx_calib_dump", "vx_plan_calibrated",
+              "vx_plan_ex_calibrated"):
         getattr(L, f).restype = ctypes.c_int
     if L.vx_abi_version() != 1:
         raise ImportError("libvx.so ABI %d != binding ABI 1 (rebuild)" % L.vx_abi_version())
@@ -141,20 +152,81 @@ def _dt_name(t) -> str:
     return {torch.bfloat16: "bf16", torch.float16: "fp16", torch.float32: "fp32"}[t.dtype]
 
 
+class Calib:
+    """An empirical-tier calibration (vx_calib_t): measured live by calibrate(), or built
+    from a dict in oracle/calib_b200.json format (from_dict)."""
+
+    def __init__(self, handle):
+        self._h = handle
+
+    @classmethod
+    def from_dict(cls, d: dict) -> "Calib":
+        h = ctypes.c_void_p()
+        _check(_lib.vx_calib_new(d["hbm_milli"], d["dsm_milli"], d["fixed_cluster"],
+                                 d["skfix_milli"], ctypes.byref(h)), "vx_calib_new")
+        c = cls(h)
+        for k, r in d["rungs"].items():
+            _check(_lib.vx_calib_set_rung(h, k.encode(), r["mac_milli"], r["l2s_milli"],
+                                          r["epi_milli"], r["fixed"]), "vx_calib_set_rung")
+        return c
+
+    def dump(self) -> dict:
+        return _calib_dump(self._h)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib is not None:
+            _lib.vx_calib_destroy(h)
+            self._h = None
+
+
+def _calib_dump(h) -> dict:
+    need = ctypes.c_size_t(0)
+    _lib.vx_calib_dump(h, None, 0, ctypes.byref(need))
+    buf = ctypes.create_string_buffer(need.value)
+    _check(_lib.vx_calib_dump(h, buf, need.value, ctypes.byref(need)), "vx_calib_dump")
+    return json.loads(buf.value.decode())
+
+
+def builtin_calib() -> dict:
+    """The compiled-in empirical tier (vx_calib.cpp) as a dict."""
+    return _calib_dump(None)
+
+
+def calibrate(device: int = 0, b_layout: str = "nk", effort: int = 0) -> Calib:
+    """Live empirical tier (vx_calibrate): profile every rung on `device` over a fixed generic
+    grid and fit the cost model's per-rung constants."""
+    h = ctypes.c_void_p()
+    _check(_lib.vx_calibrate(int(device), _BL[b_layout], int(effort), ctypes.byref(h)),
+           "vx_calibrate")
+    return Calib(h)
+
+
 class Plan:
-    """Offline strategy table for C[M,N] = A[M,K] x B (vx_plan).  N=0 means dynamic N."""
+    """Offline strategy table for C[M,N] = A[M,K] x B (vx_plan).  N=0 means dynamic N.
+    calib: an empirical tier to freeze into the plan instead of the compiled-in one."""
 
     def __init__(self, N: int, K: int, in_dtype: str = "bf16", out_dtype: str = "bf16",
-                 b_layout: str = "nk", device: int | None = 0, desc: DeviceDesc | None = None):
+                 b_layout: str = "nk", device: int | None = 0, desc: DeviceDesc | None = None,
+                 calib: "Calib | None" = None):
         self.N, self.K = int(N), int(K)
         self.in_dtype, self.out_dtype, self.b_layout = in_dtype, out_dtype, b_layout
         h = ctypes.c_void_p()
-        if desc is not None:
-            _check(_lib.vx_plan_ex(self.N, self.K, _DT[in_dtype], _DT[out_dtype], _BL[b_layout],
-                                   ctypes.byref(desc), ctypes.byref(h)), "vx_plan_ex")
+        args = (self.N, self.K, _DT[in_dtype], _DT[out_dtype], _BL[b_layout])
+        if desc is not None and calib is not None:
+            _check(_lib.vx_plan_ex_calibrated(*args, ctypes.byref(desc), calib.handle,
+                                              ctypes.byref(h)), "vx_plan_ex_calibrated")
+        elif desc is not None:
+            _check(_lib.vx_plan_ex(*args, ctypes.byref(desc), ctypes.byref(h)), "vx_plan_ex")
+        elif calib is not None:
+            _check(_lib.vx_plan_calibrated(*args, int(device), calib.handle, ctypes.byref(h)),
+                   "vx_plan_calibrated")
         else:
-            _check(_lib.vx_plan(self.N, self.K, _DT[in_dtype], _DT[out_dtype], _BL[b_layout],
-                                int(device), ctypes.byref(h)), "vx_plan")
+            _check(_lib.vx_plan(*args, int(device), ctypes.byref(h)), "vx_plan")
         self._h = h
 
     def __del__(self):

@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libvx.so")
-SOURCES = ["vx_plan.cpp", "vx_calib.cpp", "vx_dispatch.cu"]
+SOURCES = ["vx_plan.cpp", "vx_calib.cpp", "vx_dispatch.cu", "vx_live.cu"]
 HEADERS = ["vx_internal.h", "vx_ptx.cuh", "vx_umma.cuh", "vx_simt.cuh", "vx_gemv.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

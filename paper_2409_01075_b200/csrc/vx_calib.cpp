@@ -69,4 +69,15 @@ const RungCalib* calib_lookup(const std::string& key) {
 int calib_count() { return (int)(sizeof(kRungs) / sizeof(kRungs[0])); }
 const RungCalib* calib_at(int i) { return &kRungs[i]; }
 
+const CalibTable& builtin_calib() {
+    static const CalibTable t = [] {
+        CalibTable c;
+        c.glob = kCalib;
+        c.source = "compiled-in";
+        for (const auto& r : kRungs) c.rungs.push_back({r.key, r.mac_milli, r.l2s_milli, r.epi_milli, r.fixed});
+        return c;
+    }();
+    return t;
+}
+
 }  // namespace vx

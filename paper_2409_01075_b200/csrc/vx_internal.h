@@ -58,11 +58,33 @@ const RungCalib* calib_lookup(const std::string& key);
 int calib_count();
 const RungCalib* calib_at(int i);
 
+// A calibration as a plan holds it: the compiled-in one (vx_calib.cpp) or one measured live
+// on the device by vx_calibrate (vx_live.cu).  Immutable once built.
+struct RungConst {
+    std::string key;
+    int64_t mac_milli, l2s_milli, epi_milli, fixed;
+};
+struct CalibTable {
+    Calib glob;
+    std::vector<RungConst> rungs;
+    std::string source;   // "compiled-in" or "live:<device>"
+    const RungConst* find(const std::string& key) const {
+        for (const auto& r : rungs)
+            if (r.key == key) return &r;
+        return nullptr;
+    }
+};
+const CalibTable& builtin_calib();
+
 struct LevelCounts {
     int64_t l0, l1, l2, l3;
 };
 
 }  // namespace vx
+
+struct vx_calib_s {
+    vx::CalibTable table;
+};
 
 struct vx_plan_s {
     int64_t N;  // 0 = dynamic
@@ -70,6 +92,7 @@ struct vx_plan_s {
     vx_dtype in, out;
     vx_blayout bl;
     vx_device_desc desc;
+    vx::CalibTable cal;   // the empirical tier this plan's selection uses (copied, immutable)
     int device;  // -1 when built from an explicit descriptor
     std::vector<vx::Rung> rungs;
     vx::LevelCounts counts;

@@ -212,7 +212,7 @@ static vx_status build_rungs(vx_plan_s* p) {
         char key[64];
         if (r.mc > 1) snprintf(key, sizeof key, "%s_mc%d_%dx%d", family_name(r.family), r.mc, r.bm, r.bn);
         else snprintf(key, sizeof key, "%s_%dx%d", family_name(r.family), r.bm, r.bn);
-        const RungCalib* c = calib_lookup(key);
+        const RungConst* c = p->cal.find(key);
         if (!c) { set_error("no calibration for rung %s", key); return VX_ERR_UNSUPPORTED; }
         r.mac_milli = c->mac_milli; r.l2s_milli = c->l2s_milli;
         r.epi_milli = c->epi_milli; r.fixed = c->fixed;
@@ -241,7 +241,7 @@ static bool sk_admissible(const vx_plan_s* p, const Rung& r, int64_t batch, int6
 static void rung_cost(const vx_plan_s* p, const Rung& r, int s, int64_t batch, int64_t M,
                       int64_t N, vx_choice* o) {
     const vx_device_desc& d = p->desc;
-    const Calib& cal = calib_globals();
+    const Calib& cal = p->cal.glob;
     const int64_t K = p->K;
     const int in_b = in_bytes(p->in), out_b = out_bytes(p->out);
     const int64_t bm = r.bm, bn = r.bn, bk = r.bk;
@@ -450,8 +450,8 @@ const char* vx_status_str(vx_status s) {
 
 const char* vx_last_error(void) { return g_err; }
 
-vx_status vx_plan_ex(int64_t N, int64_t K, vx_dtype in, vx_dtype out, vx_blayout bl,
-                     const vx_device_desc* desc, vx_plan_t* plan) {
+static vx_status plan_create(int64_t N, int64_t K, vx_dtype in, vx_dtype out, vx_blayout bl,
+                             const vx_device_desc* desc, const CalibTable& cal, vx_plan_t* plan) {
     g_err[0] = 0;
     if (!desc || !plan) { set_error("NULL argument"); return VX_ERR_INVALID; }
     *plan = nullptr;
@@ -483,6 +483,7 @@ vx_status vx_plan_ex(int64_t N, int64_t K, vx_dtype in, vx_dtype out, vx_blayout
     std::unique_ptr<vx_plan_s> p(new (std::nothrow) vx_plan_s());
     if (!p) return VX_ERR_OOM;
     p->N = N; p->K = K; p->in = in; p->out = out; p->bl = bl; p->desc = *desc; p->device = -1;
+    p->cal = cal;
     vx_status st = build_rungs(p.get());
     if (st != VX_OK) return st;
     p->memo.resize(vx_plan_s::kMemo + 1);
@@ -490,6 +491,85 @@ vx_status vx_plan_ex(int64_t N, int64_t K, vx_dtype in, vx_dtype out, vx_blayout
     if (!p->memo_state) return VX_ERR_OOM;
     for (int64_t i = 0; i <= vx_plan_s::kMemo; ++i) p->memo_state[i].store(0);
     *plan = p.release();
+    return VX_OK;
+}
+
+vx_status vx_plan_ex(int64_t N, int64_t K, vx_dtype in, vx_dtype out, vx_blayout bl,
+                     const vx_device_desc* desc, vx_plan_t* plan) {
+    return plan_create(N, K, in, out, bl, desc, builtin_calib(), plan);
+}
+
+vx_status vx_plan_ex_calibrated(int64_t N, int64_t K, vx_dtype in, vx_dtype out, vx_blayout bl,
+                                const vx_device_desc* desc, vx_calib_t calib, vx_plan_t* plan) {
+    if (!calib) { set_error("NULL calibration"); return VX_ERR_INVALID; }
+    return plan_create(N, K, in, out, bl, desc, calib->table, plan);
+}
+
+vx_status vx_plan_calibrated(int64_t N, int64_t K, vx_dtype in, vx_dtype out, vx_blayout bl,
+                             int device, vx_calib_t calib, vx_plan_t* plan) {
+    if (!calib || !plan) { set_error("NULL argument"); return VX_ERR_INVALID; }
+    vx_device_desc d;
+    vx_status st = vx_device_probe(device, &d);
+    if (st != VX_OK) return st;
+    st = plan_create(N, K, in, out, bl, &d, calib->table, plan);
+    if (st != VX_OK) return st;
+    (*plan)->device = device;
+    st = prepare_kernels(*plan);
+    if (st != VX_OK) { vx_plan_destroy(*plan); *plan = nullptr; }
+    return st;
+}
+
+vx_status vx_calib_new(int64_t hbm_milli, int64_t dsm_milli, int64_t fixed_cluster,
+                       int64_t skfix_milli, vx_calib_t* out) {
+    if (!out) { set_error("NULL argument"); return VX_ERR_INVALID; }
+    if (hbm_milli <= 0 || dsm_milli <= 0 || fixed_cluster < 0 || skfix_milli <= 0) {
+        set_error("calibration rates must be > 0"); return VX_ERR_INVALID;
+    }
+    vx_calib_s* c = new (std::nothrow) vx_calib_s();
+    if (!c) return VX_ERR_OOM;
+    c->table.glob = {hbm_milli, dsm_milli, fixed_cluster, skfix_milli};
+    c->table.source = "user";
+    *out = c;
+    return VX_OK;
+}
+
+vx_status vx_calib_set_rung(vx_calib_t c, const char* key, int64_t mac_milli, int64_t l2s_milli,
+                            int64_t epi_milli, int64_t fixed) {
+    if (!c || !key) { set_error("NULL argument"); return VX_ERR_INVALID; }
+    if (mac_milli <= 0 || l2s_milli <= 0 || epi_milli <= 0 || fixed < 0) {
+        set_error("rung rates must be > 0"); return VX_ERR_INVALID;
+    }
+    for (auto& r : c->table.rungs)
+        if (r.key == key) { r = {key, mac_milli, l2s_milli, epi_milli, fixed}; return VX_OK; }
+    c->table.rungs.push_back({key, mac_milli, l2s_milli, epi_milli, fixed});
+    return VX_OK;
+}
+
+vx_status vx_calib_destroy(vx_calib_t c) {
+    delete c;
+    return VX_OK;
+}
+
+vx_status vx_calib_dump(vx_calib_t c, char* buf, size_t cap, size_t* need) {
+    const CalibTable& t = c ? c->table : builtin_calib();
+    std::string s;
+    char tmp[256];
+    snprintf(tmp, sizeof tmp, "{\"source\":\"%s\",\"hbm_milli\":%lld,\"dsm_milli\":%lld,"
+             "\"fixed_cluster\":%lld,\"skfix_milli\":%lld,\"rungs\":{", t.source.c_str(),
+             (long long)t.glob.hbm_milli, (long long)t.glob.dsm_milli,
+             (long long)t.glob.fixed_cluster, (long long)t.glob.skfix_milli);
+    s += tmp;
+    for (size_t i = 0; i < t.rungs.size(); ++i) {
+        const RungConst& r = t.rungs[i];
+        snprintf(tmp, sizeof tmp, "%s\"%s\":{\"mac_milli\":%lld,\"l2s_milli\":%lld,\"epi_milli\":%lld,"
+                 "\"fixed\":%lld}", i ? "," : "", r.key.c_str(), (long long)r.mac_milli,
+                 (long long)r.l2s_milli, (long long)r.epi_milli, (long long)r.fixed);
+        s += tmp;
+    }
+    s += "}}";
+    if (need) *need = s.size() + 1;
+    if (!buf || cap < s.size() + 1) { set_error("dump buffer too small"); return VX_ERR_BUFFER; }
+    memcpy(buf, s.c_str(), s.size() + 1);
     return VX_OK;
 }
 
@@ -525,7 +605,7 @@ vx_status vx_plan_dump(vx_plan_t p, char* buf, size_t cap, size_t* need) {
     if (!p) { set_error("NULL plan"); return VX_ERR_INVALID; }
     std::string s;
     char tmp[512];
-    const Calib& c = calib_globals();
+    const Calib& c = p->cal.glob;
     snprintf(tmp, sizeof tmp,
              "{\"abi\":%d,\"N\":%lld,\"K\":%lld,\"in\":\"%s\",\"out\":\"%s\",\"b_layout\":\"%s\","
              "\"levels\":{\"l0\":%lld,\"l1\":%lld,\"l2\":%lld,\"l3\":%lld},"

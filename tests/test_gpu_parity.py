@@ -530,3 +530,24 @@ def test_fused_gemm_gather_symmetric_memory_single_rank():
         assert np.array_equal(C.cpu().double().numpy(), oracle.gemm(A, B, "nk"))
     finally:
         dist.destroy_process_group()
+
+
+def test_live_calibration_freezes_into_plans():
+    """vx_calibrate: profiles every 16-bit rung on this
+    device over the fixed generic grid, fits the per-rung constants, and the frozen table
+    drives a plan whose selection is deterministic and whose results are exact."""
+    vx = vxmod()
+    c = vx.calibrate(0, "nk", effort=0)
+    d = c.dump()
+    assert d["source"].startswith("live:")
+    builtin = vx.builtin_calib()
+    assert set(d["rungs"]) == set(builtin["rungs"])
+    for k, r in d["rungs"].items():
+        assert min(r.values()) >= 0 and r["mac_milli"] > 0, k
+    p = vx.Plan(3072, 768, "bf16", "fp32", "nk", calib=c)
+    q = vx.Plan(3072, 768, "bf16", "fp32", "nk", calib=vx.Calib.from_dict(d))
+    for M in (1, 37, 512, 4096):
+        assert p.select(M) == q.select(M)          # frozen: same table -> same choice
+        A, B = synth.gemm_inputs(M, 3072, 768, "bf16", "nk", kind="int", seed=M)
+        got, _ = _run(p, A, B)
+        assert np.array_equal(got, oracle.gemm(A, B, "nk")), M

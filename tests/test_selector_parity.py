@@ -109,3 +109,49 @@ def test_forced_cost_matches_oracle():
                 a = p.cost(r["rung_id"], s, M)
                 b = S.rung_cost(r, s, 1, M, 3072, 768, "bf16", "bf16", DESC_J, CAL)
                 assert a["cost"] == b["cost"] and a["grid"] == b["grid"]
+
+
+def test_builtin_calibration_dump_matches_oracle_copy():
+    """vx_calib_dump(NULL) is the compiled-in empirical tier; the oracle's JSON copy agrees."""
+    d = vx.builtin_calib()
+    assert d["source"] == "compiled-in"
+    for k in ("hbm_milli", "dsm_milli", "fixed_cluster", "skfix_milli"):
+        assert d[k] == CAL[k]
+    for key, r in CAL["rungs"].items():
+        assert d["rungs"][key] == r, key
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_selection_parity_under_arbitrary_calibration(seed):
+    """A calibration is data (the empirical tier, live or compiled in): for a randomly
+    perturbed table handed to BOTH the library (vx_plan_ex_calibrated) and the oracle, the
+    selections agree for every M of a dense sweep -- the selector is the same function of
+    the calibration, not just of one table."""
+    import random
+    rnd = random.Random(seed)
+    cal = json.loads(json.dumps(CAL))
+    for k in ("dsm_milli", "fixed_cluster", "skfix_milli"):
+        cal[k] = max(1, int(cal[k] * rnd.uniform(0.5, 2.0)))
+    for r in cal["rungs"].values():
+        for f in ("mac_milli", "l2s_milli", "epi_milli", "fixed"):
+            r[f] = max(1, int(r[f] * rnd.uniform(0.3, 3.0)))
+    c = vx.Calib.from_dict(cal)
+    for N, K in ((3072, 768), (11008, 4096)):
+        p = vx.Plan(N, K, "bf16", "bf16", "nk", desc=DESC, calib=c)
+        d = p.dump()
+        assert d["calib"] == {k: cal[k] for k in ("hbm_milli", "dsm_milli", "fixed_cluster",
+                                                  "skfix_milli")}
+        t = _oracle_table(K, "bf16", "bf16")
+        for M in list(range(1, 600, 7)) + [1023, 1024, 4097, 16383]:
+            got = p.select(M)
+            want = S.select(t, 1, M, N, K, DESC_J, cal)
+            assert {k: got[k] for k in FIELDS} == {k: want[k] for k in FIELDS}, (seed, N, K, M)
+
+
+def test_calibration_missing_key_rejected():
+    cal = json.loads(json.dumps(CAL))
+    del cal["rungs"]["umma_128x128"]
+    c = vx.Calib.from_dict(cal)
+    with pytest.raises(vx.VxError) as e:
+        vx.Plan(3072, 768, "bf16", "bf16", "nk", desc=DESC, calib=c)
+    assert e.value.status == 2

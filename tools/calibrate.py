@@ -27,7 +27,10 @@ CAL_M = (1, 2, 4, 8, 16, 24, 32, 48, 64, 96, 128, 160, 200, 256, 320, 384, 512, 
 # small-K shapes (K <= 1024: few k-blocks, the launch-floor regime) with odd tile counts
 CAL_NK = ((1024, 1024), (4096, 1024), (2048, 4096), (8192, 4096), (6144, 2048),
           (3328, 1536), (5376, 4096), (10752, 2048), (1536, 512), (2560, 640),
-          (1280, 896), (3584, 640), (2048, 512))
+          (1280, 896), (3584, 640), (2048, 512),
+          # round 2: grids of 75-148 CTAs per wave (where back-to-back launches can no longer
+          # overlap their prologue with the previous grid) and long-K weight streams
+          (14336, 4096), (9728, 3072), (13312, 1024), (2816, 832), (1792, 832))
 CLOCK_GHZ = 1.965   # cycles of the model are SM cycles at the max clock
 
 
@@ -40,7 +43,8 @@ def measure(args):
     stream = torch.cuda.current_stream(dev)
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     out = {"desc": vx.device_probe(0).to_json(), "clock_ghz": CLOCK_GHZ, "samples": []}
-    for N, K in CAL_NK:
+    nk_list = CAL_NK[13:] if getattr(args, "only_new", False) else CAL_NK
+    for N, K in nk_list:
         p = vx.Plan(N, K, "bf16", "bf16", "nk")
         rungs = p.dump()["rungs"]
         for M in CAL_M:
@@ -444,6 +448,7 @@ def main():
     sub = ap.add_subparsers(dest="cmd")
     m = sub.add_parser("measure")
     m.add_argument("--out", default="gpurun_out/calib_raw.json")
+    m.add_argument("--only-new", action="store_true", help="only the round-2 additions to CAL_NK")
     f = sub.add_parser("fit")
     f.add_argument("raw")
     f.add_argument("--regret-weight", type=float, default=2.0)
