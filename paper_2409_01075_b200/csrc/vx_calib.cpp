@@ -24,35 +24,35 @@ namespace vx {
 static const Calib kCalib = {
     /*hbm_milli=*/3327023,   // 6543 GB/s measured copy bandwidth / 1.965 GHz
     /*dsm_milli=*/2931,      // effective in-cluster reduce rate (fitted)
-    /*fixed_cluster=*/1051,  // cluster launch + two cluster barriers (fitted)
+    /*fixed_cluster=*/2538,  // cluster launch + two cluster barriers (fitted)
     /*skfix_milli=*/13315,   // stream-K partial write + read-back (fitted)
 };
 
 static const RungCalib kRungs[] = {
     {"umma_128x64", 1000367, 46603, 8000, 7014},
-    {"umma_128x128", 1679365, 54422, 17537, 1757},
-    {"umma_128x256", 1923790, 152381, 42657, 200},
-    {"umma_256x128", 3611307, 86550, 31800, 2883},
-    {"umma_256x64", 2323400, 160000, 33190, 10650},
-    {"umma_256x256", 4096000, 160000, 62692, 1072},
-    {"umma_swap_128x16", 1000000, 33673, 8000, 4053},
-    {"umma_swap_128x32", 1000000, 45735, 10090, 4110},
-    {"umma_swap_128x64", 1183082, 53507, 11773, 2864},
-    {"umma_swap_128x128", 1597532, 86907, 16000, 1009},
+    {"umma_128x128", 1520875, 160000, 8000, 371},
+    {"umma_128x256", 1923790, 160000, 30923, 200},
+    {"umma_256x128", 3611307, 86550, 25081, 3481},
+    {"umma_256x64", 2323400, 160000, 40405, 11183},
+    {"umma_256x256", 4096000, 146087, 70638, 1233},
+    {"umma_swap_128x16", 2468107, 33673, 9200, 4053},
+    {"umma_swap_128x32", 1000000, 45735, 15471, 4110},
+    {"umma_swap_128x64", 1183082, 56182, 11212, 2864},
+    {"umma_swap_128x128", 1837162, 51409, 14512, 1635},
     // BN = 192 / swapped BN = 192, 256 (tile-boundary cliffs, R6)
-    {"umma_128x192", 1470000, 160000, 32438, 200},
-    {"umma_swap_128x192", 1738143, 132300, 32255, 338},
-    {"umma_swap_128x256", 1844329, 160000, 23044, 200},
+    {"umma_128x192", 1470000, 106501, 34060, 200},
+    {"umma_swap_128x192", 1738143, 100193, 33920, 450},
+    {"umma_swap_128x256", 1936545, 160000, 29217, 450},
     // TMA-multicast clusters
-    {"umma_mc2_128x128", 1744850, 41151, 17435, 2426},
+    {"umma_mc2_128x128", 1744850, 41151, 13097, 2547},
     {"umma_mc2_128x256", 4096000, 38348, 512000, 3025},
-    {"umma_swap_mc2_128x32", 1000000, 36759, 8762, 6343},
-    {"umma_swap_mc2_128x64", 1043084, 40140, 512000, 6776},
+    {"umma_swap_mc2_128x32", 1000000, 36759, 8000, 3330},
+    {"umma_swap_mc2_128x64", 1050000, 40140, 512000, 7115},
     {"umma_swap_mc4_128x64", 1000000, 36408, 512000, 6776},
-    {"gemv_1x8", 11796, 9609, 1000, 3022},
-    {"gemv_2x8", 9088, 43894, 1000, 3376},
-    {"gemv_4x8", 9215, 64524, 1000, 2932},
-    {"gemv_8x8", 10665, 5341, 148392, 676},
+    {"gemv_1x8", 28714, 9151, 1000, 3332},
+    {"gemv_2x8", 8243, 43894, 1000, 3215},
+    {"gemv_4x8", 8776, 64524, 1000, 2932},
+    {"gemv_8x8", 10157, 5087, 148392, 497},
     {"simt_32x32", 128000, 32000, 16000, 2000},
     {"simt_64x64", 128000, 32000, 16000, 2000},
     {"simt_128x64", 128000, 32000, 16000, 2000},

@@ -400,7 +400,15 @@ vx_status launch(const vx_plan_s* p, const vx_choice& ch, int64_t batch, int64_t
     CUtensorMap mapA, mapB;
     // A is P (box 128 rows) or Q (box BN rows); in a multicast cluster each CTA loads (and
     // multicasts) 1/mc of A's rows
-    const int a_box = (swap ? r.bn : 128) / mc;
+    int a_box = (swap ? r.bn : 128) / mc;
+    // short A boxes: on a swapped rung, an A box of >= 64 rows over an A of
+    // fewer than 16 rows streams at ~0.6x the rate (measured, N = 8192, K = 4096: swap
+    // 128x128 at M <= 15 36-37 us vs 22 us at M = 16; 23 us with the short box); a box of
+    // round_up(M, 8) rows leaves the rest of the A tile stale in SMEM, which only feeds
+    // accumulator columns >= M that are never stored.  Narrower boxes keep the (faster)
+    // two-chunk deep-K loads instead (swap 128x32: 19.4 us with them vs 22 us short).
+    const bool short_a = swap && M < 16 && mc == 1 && !pair && a_box >= 64 && !(g_dbg & 65536);
+    if (short_a) a_box = (int)((M + 7) / 8 * 8);
     s = make_map(&mapA, A, p->in, K, M, batch, K, batch > 1 ? sA : M * K, 64, a_box);
     if (s != VX_OK) return s;
     if (p->bl == VX_B_PACKED) {
@@ -449,7 +457,10 @@ vx_status launch(const vx_plan_s* p, const vx_choice& ch, int64_t batch, int64_t
     // measured, 128 x 256 (4 stages) up to 1.17x slower, pair 256 x 256 (6 stages) 1.03x
     // slower, pair 256 x 128 (8 stages) 0.86-0.90x; VX_DEBUG_FLAGS bit 4096 turns them off
     // (A/B timing only)
-    prm.kdouble = (!b_mn && p->bl != VX_B_PACKED && K % 64 == 0 && K >= 128 && mc == 1 &&
+    // bytes of A landing in each CTA's stage: the short box, else the whole A tile (a
+    // multicast cluster's sub-boxes from every CTA all land in every CTA's stage)
+    prm.a_bytes = (short_a ? a_box : (swap ? r.bn : 128)) * 64 * 2;
+    prm.kdouble = (!b_mn && p->bl != VX_B_PACKED && K % 64 == 0 && K >= 128 && mc == 1 && !short_a &&
                    r.stages >= (pair ? 8 : 6) && !(g_dbg & 4096)) ? 1 : 0;
     CUtensorMap mapA2, mapB2;
     if (prm.kdouble) {

@@ -69,6 +69,9 @@ struct UmmaParams {
     int mc;                     // TMA-multicast cluster size (1 = none): MC CTAs share the A
                                 // operand tile (P when non-swapped, Q when swapped); tiles
                                 // and num_tiles then count cluster tiles
+    int a_bytes;                // bytes of A one stage loads: the whole A tile, or for M < 16
+                                // a short box of round_up(M, 8) rows (DESIGN.md 4.1 "short
+                                // A boxes"); the tile rows past it are never stored
     int ndst;                   // fused GEMM + row all-gather: > 0 = the
                                 // epilogue writes every finished C row chunk straight from
                                 // registers into rows dst_row0 + m of each dst[d] (peer /
@@ -571,7 +574,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                         if (stage == S) { stage = 0; phase ^= 1; }
                         continue;
                     }
-                    ptx::mbar_arrive_expect_tx(&full[stage], kP + kQ);
+                    // A may arrive as a short box (M < 16): expect exactly the bytes loaded
+                    ptx::mbar_arrive_expect_tx(&full[stage], SWAP ? kP + p.a_bytes : p.a_bytes + kQ);
                     dep_wait(tile, kb, k0 + nk - kb);
                     if (!stamped && kb == k0) trace_at(p, 11);
                     if (p.bpack) {
