@@ -130,7 +130,9 @@ BK_TC = 64                                       # one 128-B swizzle row of 2-by
 SPLITS = (1, 2, 4, 8)                            # R7
 MAX_STAGES = 16                                  # R5
 SMEM_RESERVE = 2048                              # barriers + 1024-B alignment slack
-EPI_STAGING = 32768                              # epilogue: 4 warps x 2 x 4 KB TMA-store tiles
+EPI_STAGING = 32768                              # epilogue: 8 warps x 4 KB TMA-store tiles
+EPI_STAGING_LEAN = 16384                         # occupancy-2 (lean) CTAs: 4 warps x 4 KB
+CTA_SYS_SMEM = 1024                              # shared memory reserved per resident CTA
 CLUSTER_MAX = 8                                  # portable cluster size
 
 # kernels that exist in the library (the "implemented" filter, R6):
@@ -144,6 +146,8 @@ IMPL_TC = {(0, 128, 64), (0, 128, 128), (0, 128, 192), (0, 128, 256), (0, 256, 6
            (1, 128, 192), (1, 128, 256)}
 # TMA-multicast cluster kernels: (family, bm, bn, mc), mc CTAs sharing the A tile
 IMPL_MC = {(0, 128, 128, 2), (0, 128, 256, 2), (1, 128, 32, 2), (1, 128, 64, 2), (1, 128, 64, 4)}
+# occupancy-2 (lean) kernels: (family, bm, bn), two CTAs per SM (R5b)
+IMPL_LEAN = {(0, 128, 64), (1, 128, 32), (1, 128, 64)}
 MC_SIZES = (1, 2, 4)
 SIMT_TILES = ((32, 32, 2, 4), (64, 64, 4, 4), (128, 64, 8, 4))
 SIMT_BK = 16
@@ -199,14 +203,23 @@ def build_table(K: int, in_dtype: str, out_dtype: str, desc: dict, b_layout: str
             foot = S * stage_bytes + SMEM_RESERVE + EPI_STAGING
             if foot * 8 < cap:            # utilisation window [1/8, 1] (R3)
                 continue
-            l2_init.append((am, an, BK_TC, S, st))
+            l2_init.append((am, an, BK_TC, S, st, 1))
+            # occupancy-2 ring (R5b): two CTAs per SM -- half the SM's shared memory each
+            # (less the per-CTA system reserve) and half its TMEM columns
+            if cg == 1 and 2 * st * an <= desc["tmem_cols"]:
+                fit2 = (desc["smem_per_sm"] // 2 - CTA_SYS_SMEM - SMEM_RESERVE
+                        - EPI_STAGING_LEAN) // stage_bytes
+                S2 = min(MAX_STAGES, fit2)
+                foot2 = S2 * stage_bytes + SMEM_RESERVE + EPI_STAGING_LEAN
+                if 2 <= S2 < S and foot2 * 8 >= cap:
+                    l2_init.append((am, an, BK_TC, S2, st, 2))
         l2, map2 = filter_by_multiples(
             l2_init, l1,
             lambda p, c: c[0] % p[0] == 0 and c[1] % p[1] == 0 and c[4] == p[2]
             and c[2] % UMMA_K == 0)
         # ---- L3: grid schedule (swap, splits) + implemented filter -------------------
         kb = ceil_div(K, BK_TC)
-        for (bm, bn, bk, S, st) in l2:
+        for (bm, bn, bk, S, st, occ) in l2:
             cg = 2 if bm == 256 else 1
             for swap in (0, 1):
                 if cg == 2 and swap:      # cta_group::2 pair rungs are non-swapped
@@ -221,14 +234,16 @@ def build_table(K: int, in_dtype: str, out_dtype: str, desc: dict, b_layout: str
                     # whole 8-row swizzle atoms per CTA share, unpacked B
                     if st != 2:
                         continue
-                    if mc == 1 and (swap, bm, bn) not in IMPL_TC:
+                    if occ == 2 and (mc > 1 or (swap, bm, bn) not in IMPL_LEAN):
+                        continue
+                    if occ == 1 and mc == 1 and (swap, bm, bn) not in IMPL_TC:
                         continue
                     if mc > 1 and ((swap, bm, bn, mc) not in IMPL_MC or cg > 1
                                    or (bn if swap else bm) // mc % 8 != 0
                                    or b_layout == "packed"):
                         continue
-                    if mc > 1:
-                        splits = [1]      # multicast clusters run the persistent schedule
+                    if mc > 1 or occ == 2:
+                        splits = [1]      # multicast clusters and lean CTAs are persistent
                     else:
                         splits = []
                         for s in SPLITS:
@@ -240,13 +255,13 @@ def build_table(K: int, in_dtype: str, out_dtype: str, desc: dict, b_layout: str
                         splits.append(0)  # stream-K schedule over (tile, k-block) units (R19)
                     rungs.append({"family": swap, "cg": cg, "um": bm, "un": bn, "acc_stages": st,
                                   "bm": bm, "bn": bn, "bk": bk, "stages": S, "swap": swap,
-                                  "mc": mc, "splits": splits})
+                                  "mc": mc, "occ": occ, "splits": splits})
         # adaptive backend (R20): CUDA-core rungs join the same argmin
         if b_layout != "packed":
             for mt in GEMV_MT:
                 rungs.append({"family": 3, "cg": 1, "um": 1, "un": 1, "acc_stages": 1,
                               "bm": mt, "bn": GEMV_COLS, "bk": GEMV_BK, "stages": 1, "swap": 0,
-                              "mc": 1, "splits": [1]})
+                              "mc": 1, "occ": 1, "splits": [1]})
         counts = {"l0": len(l0), "l1": len(l1), "l2": len(l2), "l3": len(rungs)}
     elif in_dtype == "fp32":
         # CUDA-core mode: L0 = FFMA thread tiles, L2 = CTA tiles
@@ -264,12 +279,13 @@ def build_table(K: int, in_dtype: str, out_dtype: str, desc: dict, b_layout: str
         for (bm, bn, bk, tm, tn) in l2:
             rungs.append({"family": 2, "cg": 1, "um": tm, "un": tn, "acc_stages": 1,
                           "bm": bm, "bn": bn, "bk": bk, "stages": 2, "swap": 0,
-                          "mc": 1, "splits": [1]})
+                          "mc": 1, "occ": 1, "splits": [1]})
         counts = {"l0": len(l0), "l1": len(l0), "l2": len(l2), "l3": len(rungs)}
     else:
         raise ValueError(in_dtype)
     # deterministic rung ids (R13): lexicographic on (family, bm, bn, stages, swap, mc)
-    rungs.sort(key=lambda r: (r["family"], r["bm"], r["bn"], r["stages"], r["swap"], r["mc"]))
+    rungs.sort(key=lambda r: (r["family"], r["bm"], r["bn"], r["stages"], r["swap"], r["mc"],
+                              r["occ"]))
     for i, r in enumerate(rungs):
         r["rung_id"] = i
     return {"K": K, "in": in_dtype, "out": out_dtype, "levels": counts, "rungs": rungs}
@@ -282,6 +298,8 @@ def build_table(K: int, in_dtype: str, out_dtype: str, desc: dict, b_layout: str
 def _calib_key(rung: dict) -> str:
     """Calibration-table key of a rung: family, TMA-multicast cluster size, tile."""
     fam = FAMILY_NAMES[rung["family"]]
+    if rung.get("occ", 1) == 2:
+        return "%s_o2_%dx%d" % (fam, rung["bm"], rung["bn"])
     if rung.get("mc", 1) > 1:
         return "%s_mc%d_%dx%d" % (fam, rung["mc"], rung["bm"], rung["bn"])
     return "%s_%dx%d" % (fam, rung["bm"], rung["bn"])

@@ -38,7 +38,15 @@ static bool mc_available(int family, int bm, int bn, int mc) {
     return false;
 }
 
-bool kernel_available(int family, int bm, int bn, int mc) {
+// occupancy-2 (lean) rungs: 128 x 64 non-swapped, swapped 128 x {32, 64}
+static bool lean_available(int family, int bm, int bn) {
+    if (family == kUmma) return bm == 128 && bn == 64;
+    if (family == kUmmaSwap) return bm == 128 && (bn == 32 || bn == 64);
+    return false;
+}
+
+bool kernel_available(int family, int bm, int bn, int mc, int occ) {
+    if (occ == 2) return mc == 1 && lean_available(family, bm, bn);
     if (mc != 1) return mc_available(family, bm, bn, mc);
     if (family == kUmma)
         return (bm == 128 && (bn == 64 || bn == 128 || bn == 192 || bn == 256)) ||
@@ -76,7 +84,20 @@ static UmmaFn pick_mc(bool b_mn) {
                 : (UmmaFn)vx_umma_kernel<BN, false, false, false, false, MC>;
 }
 
-static UmmaFn umma_fn(int family, int bm, int bn, bool b_mn, int mc = 1) {
+template <int BN, bool SWAP>
+static UmmaFn pick_lean(bool b_mn) {
+    if (SWAP) return b_mn ? (UmmaFn)vx_umma_kernel<BN, true, true, false, false, 1, true>
+                          : (UmmaFn)vx_umma_kernel<BN, true, false, false, false, 1, true>;
+    return b_mn ? (UmmaFn)vx_umma_kernel<BN, false, false, true, false, 1, true>
+                : (UmmaFn)vx_umma_kernel<BN, false, false, false, false, 1, true>;
+}
+
+static UmmaFn umma_fn(int family, int bm, int bn, bool b_mn, int mc = 1, int occ = 1) {
+    if (occ == 2) {
+        if (mc != 1 || !lean_available(family, bm, bn)) return nullptr;
+        if (family == kUmma) return pick_lean<64, false>(b_mn);
+        return bn == 32 ? pick_lean<32, true>(b_mn) : pick_lean<64, true>(b_mn);
+    }
     if (mc > 1) {
         if (!mc_available(family, bm, bn, mc)) return nullptr;
         if (family == kUmma) return bn == 128 ? pick_mc<128, false, 2>(b_mn) : pick_mc<256, false, 2>(b_mn);
@@ -124,9 +145,10 @@ static SimtFn simt_fn(int bm, int bn, int* threads) {
 }
 
 // per-CTA dynamic shared memory: S stages of (128 A rows + this CTA's B rows) x 128 B
-static int64_t umma_smem_bytes(int bm, int bn, int stages) {
+static int64_t umma_smem_bytes(int bm, int bn, int stages, int occ = 1) {
     const int cg = bm == 256 ? 2 : 1;
-    return (int64_t)stages * (bm / cg + bn / cg) * kBkTc * 2 + kSmemReserve + kEpiStaging;
+    return (int64_t)stages * (bm / cg + bn / cg) * kBkTc * 2 + kSmemReserve +
+           (occ == 2 ? kEpiStagingLean : kEpiStaging);
 }
 
 static vx_status cuda_fail(cudaError_t e, const char* what) {
@@ -390,9 +412,9 @@ vx_status launch(const vx_plan_s* p, const vx_choice& ch, int64_t batch, int64_t
     const bool b_mn = p->bl == VX_B_KN;
     const bool pair = r.cg == 2;
     const int mc = r.mc;
-    UmmaFn fn = umma_fn(r.family, r.bm, r.bn, b_mn, mc);
+    UmmaFn fn = umma_fn(r.family, r.bm, r.bn, b_mn, mc, r.occ);
     if (!fn) { set_error("no tcgen05 kernel for rung %d", r.rung_id); return VX_ERR_UNSUPPORTED; }
-    const int64_t smem = umma_smem_bytes(r.bm, r.bn, r.stages);
+    const int64_t smem = umma_smem_bytes(r.bm, r.bn, r.stages, r.occ);
     vx_status s = ensure_attr((const void*)fn, smem);
     if (s != VX_OK) return s;
 
@@ -506,7 +528,7 @@ vx_status launch(const vx_plan_s* p, const vx_choice& ch, int64_t batch, int64_t
 
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)ch.grid, 1, 1);
-    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.blockDim = dim3(r.occ == 2 ? 192 : kThreads, 1, 1);   // lean CTAs: 6 warps
     cfg.dynamicSmemBytes = (size_t)smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[2];
@@ -547,9 +569,9 @@ vx_status prepare_kernels(const vx_plan_s* p) {
     }
     for (const vx::Rung& r : p->rungs) {
         if (r.family == kSimt) continue;
-        UmmaFn fn = umma_fn(r.family, r.bm, r.bn, p->bl == VX_B_KN, r.mc);
+        UmmaFn fn = umma_fn(r.family, r.bm, r.bn, p->bl == VX_B_KN, r.mc, r.occ);
         if (!fn) continue;
-        vx_status s = ensure_attr((const void*)fn, umma_smem_bytes(r.bm, r.bn, r.stages));
+        vx_status s = ensure_attr((const void*)fn, umma_smem_bytes(r.bm, r.bn, r.stages, r.occ));
         if (s != VX_OK) return s;
     }
     return VX_OK;

@@ -20,7 +20,9 @@ constexpr int kBkTc = 64;          // one 128-B swizzle row of 2-byte elements
 constexpr int kUmmaK = 16;         // kind::f16 instruction K
 constexpr int kMaxStages = 16;     // R5
 constexpr int kSmemReserve = 2048; // barriers + 1024-B alignment slack
-constexpr int kEpiStaging = 32768; // epilogue: 4 warps x 2 x 4 KB TMA-store staging tiles
+constexpr int kEpiStaging = 32768; // epilogue: 8 warps x 4 KB TMA-store staging tiles
+constexpr int kEpiStagingLean = 16384;  // occupancy-2 (lean) CTAs: 4 epilogue warps x 4 KB
+constexpr int kCtaSysSmem = 1024;  // shared memory the system reserves per resident CTA
 constexpr int kClusterMax = 8;     // portable cluster size
 constexpr int kSimtBk = 16;
 constexpr int kGemvBk = 1024;       // k per CTA step (4 K-slice warps x 32 lanes x 8 elements)
@@ -38,6 +40,7 @@ struct Rung {
     int32_t stages;      // L2: SMEM pipeline depth
     int32_t swap;        // L3: operand swap
     int32_t mc;          // L3: TMA-multicast cluster size sharing the A tile (1 = none)
+    int32_t occ;         // L2: resident CTAs per SM the ring is sized for (1, or 2 = lean)
     std::vector<int32_t> splits;  // L3: admissible K-loop splits
     // calibration (empirical tier), scaled x1000
     int64_t mac_milli, l2s_milli, epi_milli, fixed;

@@ -58,7 +58,8 @@ const char* fam_name(int f) { return f == kUmma ? "umma" : f == kUmmaSwap ? "umm
 
 std::string key_of(const Rung& r) {
     char k[64];
-    if (r.mc > 1) snprintf(k, sizeof k, "%s_mc%d_%dx%d", fam_name(r.family), r.mc, r.bm, r.bn);
+    if (r.occ == 2) snprintf(k, sizeof k, "%s_o2_%dx%d", fam_name(r.family), r.bm, r.bn);
+    else if (r.mc > 1) snprintf(k, sizeof k, "%s_mc%d_%dx%d", fam_name(r.family), r.mc, r.bm, r.bn);
     else snprintf(k, sizeof k, "%s_%dx%d", fam_name(r.family), r.bm, r.bn);
     return k;
 }

@@ -26,7 +26,7 @@
 
 namespace vx {
 
-bool kernel_available(int family, int bm, int bn, int mc = 1);  // vx_dispatch.cu
+bool kernel_available(int family, int bm, int bn, int mc = 1, int occ = 1);  // vx_dispatch.cu
 
 static thread_local char g_err[512] = "";
 
@@ -57,7 +57,7 @@ namespace {
 
 struct L0 { int um, un, uk; };
 struct L1 { int am, an, st; };
-struct L2 { int bm, bn, bk, S, st; };
+struct L2 { int bm, bn, bk, S, st, occ; };
 
 const int kUmLattice[] = {64, 128, 256};                  // R1
 const int kNLattice[] = {8, 16, 32, 64, 128, 192, 256};   // R1
@@ -124,7 +124,17 @@ static vx_status build_rungs(vx_plan_s* p) {
             if (S < 2) continue;
             int64_t foot = S * stage + kSmemReserve + kEpiStaging;
             if (foot * 8 < d.smem_optin) continue;
-            l2i.push_back({a.am, a.an, kBkTc, S, a.st});
+            l2i.push_back({a.am, a.an, kBkTc, S, a.st, 1});
+            // occupancy-2 ring (R5b): sized so two CTAs share an SM -- half the SM's shared
+            // memory each (less the per-CTA system reserve) and half its TMEM columns -- so a
+            // launch's CTAs become resident while the previous grid still runs
+            if (cg == 1 && 2 * a.st * a.an <= d.tmem_cols) {
+                int64_t fit2 = (d.smem_per_sm / 2 - kCtaSysSmem - kSmemReserve - kEpiStagingLean) / stage;
+                int S2 = (int)std::min<int64_t>(kMaxStages, fit2);
+                int64_t foot2 = S2 * stage + kSmemReserve + kEpiStagingLean;
+                if (S2 >= 2 && S2 < S && foot2 * 8 >= d.smem_optin)
+                    l2i.push_back({a.am, a.an, kBkTc, S2, a.st, 2});
+            }
         }
         std::vector<L2> l2 = sieve(l2i, l1, [](const L1& a, const L2& c) {
             return c.bm % a.am == 0 && c.bn % a.an == 0 && c.st == a.st && c.bk % kUmmaK == 0; },
@@ -144,7 +154,8 @@ static vx_status build_rungs(vx_plan_s* p) {
                 // multicast sub-box (A rows / mc) must be whole 8-row swizzle atoms and a
                 // packed B keeps its own 5-D load path, so multicast needs B unpacked
                 for (int mc : {1, 2, 4}) {
-                    if (c.st != 2 || !kernel_available(fam, c.bm, c.bn, mc)) continue;
+                    if (c.st != 2 || !kernel_available(fam, c.bm, c.bn, mc, c.occ)) continue;
+                    if (c.occ == 2 && mc > 1) continue;   // lean CTAs are not clustered
                     if (mc > 1 && (cg > 1 || (swap ? c.bn : c.bm) / mc % 8 != 0 ||
                                    p->bl == VX_B_PACKED))
                         continue;
@@ -152,6 +163,12 @@ static vx_status build_rungs(vx_plan_s* p) {
                     r.family = fam; r.cg = cg; r.um = c.bm; r.un = c.bn; r.acc_stages = c.st;
                     r.bm = c.bm; r.bn = c.bn; r.bk = c.bk; r.stages = c.S; r.swap = swap;
                     r.mc = mc;
+                    r.occ = c.occ;
+                    if (mc > 1 || c.occ == 2) {   // multicast clusters and lean CTAs run
+                        r.splits = {1};           // the persistent schedule
+                        rungs.push_back(r);
+                        continue;
+                    }
                     if (mc > 1) {
                         r.splits = {1};     // multicast clusters run the persistent schedule
                         rungs.push_back(r);
@@ -175,7 +192,7 @@ static vx_status build_rungs(vx_plan_s* p) {
                 Rung r{};
                 r.family = kGemv; r.cg = 1; r.um = 1; r.un = 1; r.acc_stages = 1;
                 r.bm = mt; r.bn = kGemvColsPerCta; r.bk = kGemvBk; r.stages = 1; r.swap = 0;
-                r.mc = 1;
+                r.mc = 1; r.occ = 1;
                 r.splits = {1};
                 rungs.push_back(r);
             }
@@ -196,7 +213,7 @@ static vx_status build_rungs(vx_plan_s* p) {
             Rung r{};
             r.family = kSimt; r.cg = 1; r.um = t.tm; r.un = t.tn; r.acc_stages = 1;
             r.bm = t.bm; r.bn = t.bn; r.bk = kSimtBk; r.stages = 2; r.swap = 0;
-            r.mc = 1;
+            r.mc = 1; r.occ = 1;
             r.splits = {1};
             rungs.push_back(r);
         }
@@ -204,13 +221,14 @@ static vx_status build_rungs(vx_plan_s* p) {
     }
     // deterministic ids (R13)
     std::sort(rungs.begin(), rungs.end(), [](const Rung& a, const Rung& b) {
-        return std::tie(a.family, a.bm, a.bn, a.stages, a.swap, a.mc) <
-               std::tie(b.family, b.bm, b.bn, b.stages, b.swap, b.mc); });
+        return std::tie(a.family, a.bm, a.bn, a.stages, a.swap, a.mc, a.occ) <
+               std::tie(b.family, b.bm, b.bn, b.stages, b.swap, b.mc, b.occ); });
     for (size_t i = 0; i < rungs.size(); ++i) {
         Rung& r = rungs[i];
         r.rung_id = (int32_t)i;
         char key[64];
-        if (r.mc > 1) snprintf(key, sizeof key, "%s_mc%d_%dx%d", family_name(r.family), r.mc, r.bm, r.bn);
+        if (r.occ == 2) snprintf(key, sizeof key, "%s_o2_%dx%d", family_name(r.family), r.bm, r.bn);
+        else if (r.mc > 1) snprintf(key, sizeof key, "%s_mc%d_%dx%d", family_name(r.family), r.mc, r.bm, r.bn);
         else snprintf(key, sizeof key, "%s_%dx%d", family_name(r.family), r.bm, r.bn);
         const RungConst* c = p->cal.find(key);
         if (!c) { set_error("no calibration for rung %s", key); return VX_ERR_UNSUPPORTED; }
@@ -619,9 +637,9 @@ vx_status vx_plan_dump(vx_plan_t p, char* buf, size_t cap, size_t* need) {
         const Rung& r = p->rungs[i];
         snprintf(tmp, sizeof tmp,
                  "%s{\"rung_id\":%d,\"family\":%d,\"cg\":%d,\"um\":%d,\"un\":%d,\"acc_stages\":%d,"
-                 "\"bm\":%d,\"bn\":%d,\"bk\":%d,\"stages\":%d,\"swap\":%d,\"mc\":%d,\"splits\":[",
+                 "\"bm\":%d,\"bn\":%d,\"bk\":%d,\"stages\":%d,\"swap\":%d,\"mc\":%d,\"occ\":%d,\"splits\":[",
                  i ? "," : "", r.rung_id, r.family, r.cg, r.um, r.un, r.acc_stages, r.bm, r.bn,
-                 r.bk, r.stages, r.swap, r.mc);
+                 r.bk, r.stages, r.swap, r.mc, r.occ);
         s += tmp;
         for (size_t j = 0; j < r.splits.size(); ++j) {
             snprintf(tmp, sizeof tmp, "%s%d", j ? "," : "", r.splits[j]);

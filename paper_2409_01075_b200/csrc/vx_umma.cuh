@@ -156,8 +156,9 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 __device__ __forceinline__ void st_release(int* p, int v) {
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-__device__ __forceinline__ void epi_bar() {   // named barrier over the 8 epilogue warps
-    asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+template <int ET = kEpiThreads>
+__device__ __forceinline__ void epi_bar() {   // named barrier over the epilogue warps
+    asm volatile("bar.sync 1, %0;" ::"n"(ET) : "memory");
 }
 
 constexpr int kTraceSlots = 40;
@@ -358,9 +359,9 @@ __device__ __forceinline__ void add_partials(uint32_t* v, const float* ws, int c
 
 // stream-K: every epilogue warp has consumed slots c0..c1 -> clear their flags for the next
 // launch (each slot is produced and consumed exactly once per launch)
-template <bool PAIR>
+template <bool PAIR, int ET = kEpiThreads>
 __device__ __forceinline__ void sk_reset(const UmmaParams& p, int c0, int c1, uint32_t rank) {
-    epi_bar();
+    epi_bar<ET>();
     if (threadIdx.x == kEpiWarp0 * 32)
         for (int j = c0; j <= c1; ++j) p.flags[sk_slot<PAIR>(j, rank)] = 0;
 }
@@ -372,8 +373,12 @@ __device__ __forceinline__ void sk_reset(const UmmaParams& p, int c0, int c1, ui
 // MC: TMA-multicast cluster of MC CTAs sharing the A tile (persistent schedule only): each
 // CTA loads 1/MC of the shared tile's rows and multicasts them to the whole cluster; a
 // stage is refilled only when all MC CTAs' MMAs released it (empty barriers count MC).
-template <int BN, bool SWAP, bool P_MN, bool Q_MN, bool PAIR = false, int MC = 1>
-__global__ void __launch_bounds__(kThreads, 1)
+// LEAN: occupancy-2 variant (DESIGN.md 4.1 "lean CTAs"): 1 producer + 1 MMA + 4 epilogue
+// warps (192 threads, <= 170 registers) and a ring of <= ~110 KB, so two CTAs fit on an SM
+// and a launch's CTAs become resident while the previous grid on the stream still holds its
+// SMs (programmatic dependent launch overlaps their prologue on every SM)
+template <int BN, bool SWAP, bool P_MN, bool Q_MN, bool PAIR = false, int MC = 1, bool LEAN = false>
+__global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
     vx_umma_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmQ,
                    const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmP2,
                    const __grid_constant__ CUtensorMap tmQ2, const __grid_constant__ UmmaParams p) {
@@ -381,6 +386,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     static_assert(MC == 1 || !PAIR, "multicast clusters are cta_group::1");
     static_assert(MC == 1 || (SWAP ? BN / MC : 128 / MC) % 8 == 0,
                   "multicast sub-boxes are whole 8-row swizzle atoms");
+    static_assert(!LEAN || (!PAIR && MC == 1 && BN <= 128), "lean CTAs: cta_group::1, BN <= 128");
+    constexpr int EW = LEAN ? 4 : kEpiWarps;    // epilogue warps
+    constexpr int ET = EW * 32;
+    constexpr int NG = EW / 4;                  // epilogue warps per TMEM lane quarter
+    constexpr int PW = LEAN ? 1 : kProdWarps;   // TMA producer warps
+    constexpr int PW1 = kEpiWarp0 + EW;         // the second producer warp (PW == 2)
     constexpr bool MCP = MC > 1 && !SWAP;   // A = P is the multicast operand
     constexpr bool MCQ = MC > 1 && SWAP;    // A = Q is the multicast operand
     constexpr uint16_t kMcMask = (uint16_t)((1u << MC) - 1);
@@ -422,7 +433,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(&tfull[i], 1);
-            ptx::mbar_init(&tempty[i], PAIR ? 2 * kEpiWarps : kEpiWarps);
+            ptx::mbar_init(&tempty[i], PAIR ? 2 * EW : EW);
         }
         ptx::mbar_init(redbar, 1);
         ptx::fence_mbar_init();
@@ -453,7 +464,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int rank = split ? (int)(blockIdx.x % p.splits) : 0;
     const int tile0 = split ? (int)(blockIdx.x / p.splits) : (int)blockIdx.x;  // split mode
 
-    if (warp == 0 || warp == kProdWarp1) {
+    if (warp == 0 || (PW > 1 && warp == PW1)) {
         if (lane == 0) {
             // ===== TMA producers: producer `pid` takes this CTA's k-blocks j % 2 == pid =====
             const int pid = warp == 0 ? 0 : 1;
@@ -504,7 +515,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     // range lands in the next ring stage without a wrap; the MMA issuer walks
                     // the same rule; j counts units, alternating between the producers
                     const bool dbl = kd && kb + 1 < k0 + nk && stage + 1 < S;
-                    if (j % kProdWarps != pid) {
+                    if (j % PW != pid) {
                         if (dbl) { ++kb; ++stage; }
                         if (++stage == S) { stage = 0; phase ^= 1; }
                         continue;
@@ -512,7 +523,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
                     if (dbl) ptx::mbar_wait(&empty[stage + 1], phase ^ 1);
                     if (j == 0) cyc_at(p, 23, cy0);
-                    if (kb >= k0 + kProdWarps && !stamped) { trace_at(p, 10); stamped = true; }
+                    if (kb >= k0 + PW && !stamped) { trace_at(p, 10); stamped = true; }
                     uint8_t* dP = sP + stage * kP;
                     uint8_t* dQ = sQ + stage * kQ;
                     if (PAIR && dbl) {
@@ -720,7 +731,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
         }
-    } else if (is_epi_warp(warp)) {
+    } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + EW) {
         // ===== epilogue warps =====
         ptx::grid_dep_wait();
         // warp w reads TMEM lanes 32*(w%4)..+31 (its quarter of the tile rows); the two
@@ -771,7 +782,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             if (++spins > 4) __nanosleep(32);
                     }
                 }
-                epi_bar();
+                epi_bar<ET>();
                 if (st1) cyc_at(p, 32, cyt0);
             }
             const int acc = it & 1;
@@ -792,7 +803,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // slot layout [col/4][row][4] (coalesced across the warp's rows)
                 float* slot = p.ws + (long long)blockIdx.x * 128 * BN + (long long)row * 4;
 #pragma unroll 1
-                for (int c = grp; c < (BN + 31) / 32; c += 2) {
+                for (int c = grp; c < (BN + 31) / 32; c += NG) {
                     uint32_t v[32];
                     if (BN >= 32) ptx::tmem_ld32(taddr + c * 32, v);
                     else ptx::tmem_ld16(taddr + c * 32, v);
@@ -809,7 +820,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // publish: every epilogue thread's partial stores, then the named barrier,
                 // then ONE thread's gpu-scope fence + release store of the flag (cumulative
                 // over the stores the barrier ordered before it)
-                epi_bar();
+                epi_bar<ET>();
                 if (threadIdx.x == kEpiWarp0 * 32) {
                     __threadfence();
                     st_release(p.flags + blockIdx.x, 1);
@@ -824,7 +835,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int CW = 128 / ob;                  // columns per 128-B row
                     const uint32_t rowa = wbuf + (uint32_t)lane * 128u;
 #pragma unroll 1
-                    for (int k = grp; k < BN / CW; k += 2) {
+                    for (int k = grp; k < BN / CW; k += NG) {
                         if (pending) {
                             if (lane == 0) ptx::bulk_wait_read<0>();
                             __syncwarp();
@@ -865,7 +876,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 } else {
                     constexpr int W = BN >= 32 ? 32 : BN;     // m values per chunk
 #pragma unroll 1
-                    for (int c = grp; c < BN / W; c += 2) {
+                    for (int c = grp; c < BN / W; c += NG) {
                         if (pending) {
                             if (lane == 0) ptx::bulk_wait_read<0>();
                             __syncwarp();
@@ -904,14 +915,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) release_acc(&tempty[acc]);
-                if (c_last >= c_first) sk_reset<PAIR>(p, c_first, c_last, prank);
+                if (c_last >= c_first) sk_reset<PAIR, ET>(p, c_first, c_last, prank);
                 continue;
             }
             const int pr = prow0 + row;  // global index on the P axis
             char* Cb = reinterpret_cast<char*>(p.C) +
                        (long long)b * p.sC * (p.out_kind == 2 ? 4 : 2);
 #pragma unroll 1
-            for (int c = grp; c < (BN + 31) / 32; c += 2) {
+            for (int c = grp; c < (BN + 31) / 32; c += NG) {
                 uint32_t v[32];
                 if (BN >= 32) ptx::tmem_ld32(taddr + c * 32, v);
                 else ptx::tmem_ld16(taddr + c * 32, v);
@@ -950,7 +961,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) release_acc(&tempty[acc]);
-            if (c_last >= c_first) sk_reset<PAIR>(p, c_first, c_last, prank);
+            if (c_last >= c_first) sk_reset<PAIR, ET>(p, c_first, c_last, prank);
         }
         // TMA stores have read their staging before the CTA retires (the grid completes only
         // once the stores are performed, which is what the next grid's wait observes)
@@ -991,7 +1002,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tc_fence_after();
         if (threadIdx.x == kEpiWarp0 * 32) trace_at(p, 16);
         const long long cyp = clock64();
-        if (is_epi_warp(warp) && post) {
+        if (warp >= kEpiWarp0 && warp < kEpiWarp0 + EW && post) {
             const int quarter = warp & 3;
             const int row = quarter * 32 + lane;
             const int owner = row / rows;
@@ -1003,7 +1014,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int grp = (warp - kEpiWarp0) >> 2;
             const int sw = G == 8 ? (rr & 7) : G == 4 ? ((rr >> 1) & 3) : 0;
 #pragma unroll 1
-            for (int c = grp; c < (BN + 31) / 32; c += 2) {
+            for (int c = grp; c < (BN + 31) / 32; c += NG) {
                 uint32_t v[32];
                 if (BN >= 32) ptx::tmem_ld32(taddr + c * 32, v);
                 else ptx::tmem_ld16(taddr + c * 32, v);
@@ -1018,14 +1029,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
         if (threadIdx.x == kEpiWarp0 * 32) { trace_at(p, 17); cyc_at(p, 30, cyp); }
-        if (is_epi_warp(warp)) {
-            epi_bar();                               // this CTA's own rows are in SMEM
+        if (warp >= kEpiWarp0 && warp < kEpiWarp0 + EW) {
+            epi_bar<ET>();                           // this CTA's own rows are in SMEM
             if (threadIdx.x == kEpiWarp0 * 32) cyc_at(p, 19, cyp);
             if (post) ptx::mbar_wait(redbar, 0);     // the peers' rows too
         }
         if (threadIdx.x == kEpiWarp0 * 32) trace_at(p, 6);
         cyr = clock64();
-        if (is_epi_warp(warp) && !(p.dbg & 2)) {
+        if (warp >= kEpiWarp0 && warp < kEpiWarp0 + EW && !(p.dbg & 2)) {
             int b, tp, tq;
             decode_tile(tile0, p.tiles_p, p.tiles_q, b, tp, tq);
             const int et = threadIdx.x - kEpiWarp0 * 32;
@@ -1034,7 +1045,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                        (long long)b * p.sC * (p.out_kind == 2 ? 4 : 2);
             const int n4 = BN / 4;
 #pragma unroll 1
-            for (int idx = et; idx < rows * n4; idx += kEpiThreads) {
+            for (int idx = et; idx < rows * n4; idx += ET) {
                 int rr, cc;
                 if (SWAP) { rr = idx % rows; cc = (idx / rows) * 4; }   // consecutive n
                 else { rr = idx / n4; cc = (idx % n4) * 4; }            // consecutive n

@@ -51,6 +51,8 @@ def test_simt_slots_worked_examples(case):
 
 def _key(r):
     fam = "umma_swap" if r["swap"] else "umma"
+    if r.get("occ", 1) == 2:
+        return "%s_o2_%dx%d" % (fam, r["bm"], r["bn"])
     return "%s_%dx%d" % (fam, r["bm"], r["bn"])
 
 
@@ -60,7 +62,7 @@ def test_stage_counts_b200():
     t = S.build_table(4096, "bf16", "bf16", B200)
     seen = {}
     for r in t["rungs"]:
-        if r["family"] in (0, 1):
+        if r["family"] in (0, 1) and r["mc"] == 1:
             seen[_key(r)] = r["stages"]
     assert seen == CV["stages_b200"]
 
@@ -70,7 +72,7 @@ def test_stage_counts_small_smem_and_drop_rule():
     half of that get S < 2 and are dropped (R5)."""
     d = dict(B200, smem_optin=100000)
     t = S.build_table(4096, "bf16", "bf16", d)
-    seen = {_key(r): r["stages"] for r in t["rungs"] if r["family"] in (0, 1)}
+    seen = {_key(r): r["stages"] for r in t["rungs"] if r["family"] in (0, 1) and r["mc"] == 1}
     want = CV["stages_smem100k"]
     for k, v in want.items():
         if k == "dropped":

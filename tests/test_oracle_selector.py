@@ -101,7 +101,14 @@ def test_table_invariants(K):
         foot = r["stages"] * (r["bm"] // cg + r["bn"] // cg) * r["bk"] * 2 + S.SMEM_RESERVE + S.EPI_STAGING
         assert foot <= DESC["smem_optin"] and r["stages"] >= 2
         assert r["acc_stages"] * r["bn"] <= DESC["tmem_cols"]
-        # split-K slices are whole k-blocks; multicast clusters are persistent
+        # split-K slices are whole k-blocks; multicast clusters and
+        # occupancy-2 (lean) CTAs are persistent
+        if r["occ"] == 2:
+            assert r["splits"] == [1] and r["cg"] == 1 and r["mc"] == 1
+            foot = r["stages"] * (r["bm"] + r["bn"]) * r["bk"] * 2 + S.SMEM_RESERVE + S.EPI_STAGING_LEAN
+            assert 2 * (foot + S.CTA_SYS_SMEM) <= DESC["smem_per_sm"]       # two CTAs per SM
+            assert 2 * r["acc_stages"] * r["bn"] <= DESC["tmem_cols"]
+            continue
         if r["mc"] > 1:
             assert r["splits"] == [1] and r["cg"] == 1
             assert (r["bn"] if r["swap"] else r["bm"]) // r["mc"] % 8 == 0   # whole swizzle atoms

@@ -29,7 +29,7 @@ def _oracle_table(K, i, o, bl="nk"):
 
 def _lib_rungs(dump):
     keep = ("rung_id", "family", "cg", "um", "un", "acc_stages", "bm", "bn", "bk", "stages",
-            "swap", "splits")
+            "swap", "mc", "occ", "splits")
     return [{k: r[k] for k in keep} for r in dump["rungs"]]
 
 
@@ -41,7 +41,7 @@ def test_tables_identical(K, io):
     t = _oracle_table(K, io[0], io[1])
     assert d["levels"] == t["levels"]
     want = [{k: r[k] for k in ("rung_id", "family", "cg", "um", "un", "acc_stages", "bm", "bn",
-                               "bk", "stages", "swap", "splits")} for r in t["rungs"]]
+                               "bk", "stages", "swap", "mc", "occ", "splits")} for r in t["rungs"]]
     assert _lib_rungs(d) == want
 
 

@@ -55,7 +55,8 @@ def measure(args):
                     t = time_graph(p, 1, M, N, K, r["rung_id"], s, dev, stream, l2, 3, "nk")
                     out["samples"].append({"M": M, "N": N, "K": K, "rung": r["rung_id"],
                                            "family": r["family"], "bm": r["bm"], "bn": r["bn"],
-                                           "mc": r.get("mc", 1), "stages": r["stages"],
+                                           "mc": r.get("mc", 1), "occ": r.get("occ", 1),
+                                           "stages": r["stages"],
                                            "split": s, "us": t})
             print("N=%d K=%d M=%d done" % (N, K, M), flush=True)
     json.dump(out, open(args.out, "w"))
@@ -66,8 +67,10 @@ def _cd(a, b):
     return -(-a // b)
 
 
-def calib_key(fam, bm, bn, mc=1):
+def calib_key(fam, bm, bn, mc=1, occ=1):
     """Calibration-table key of a rung (the library's vx_plan.cpp naming)."""
+    if occ == 2:
+        return "%s_o2_%dx%d" % (fam, bm, bn)
     return "%s_mc%d_%dx%d" % (fam, mc, bm, bn) if mc > 1 else "%s_%dx%d" % (fam, bm, bn)
 
 
@@ -147,7 +150,7 @@ def fit(args):
     desc = raw["desc"]
     S = raw["samples"]
     fam = {0: "umma", 1: "umma_swap", 3: "gemv"}
-    keys = sorted({(fam[x["family"]], x["bm"], x["bn"], x.get("mc", 1)) for x in S})
+    keys = sorted({(fam[x["family"]], x["bm"], x["bn"], x.get("mc", 1), x.get("occ", 1)) for x in S})
     ini0 = json.load(open(args.init)) if args.init else None
     names = [calib_key(*k) for k in keys]
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -177,7 +180,7 @@ def fit(args):
         return th, g
 
     def key_of(x):
-        return calib_key(fam[x["family"]], x["bm"], x["bn"], x.get("mc", 1))
+        return calib_key(fam[x["family"]], x["bm"], x["bn"], x.get("mc", 1), x.get("occ", 1))
 
     groups = {}
     for sm in S:
@@ -288,7 +291,7 @@ def fit_fast(args):
     desc = raw["desc"]
     S = raw["samples"]
     fam = {0: "umma", 1: "umma_swap", 3: "gemv"}
-    keys = sorted({(fam[x["family"]], x["bm"], x["bn"], x.get("mc", 1)) for x in S})
+    keys = sorted({(fam[x["family"]], x["bm"], x["bn"], x.get("mc", 1), x.get("occ", 1)) for x in S})
     names = [calib_key(*k) for k in keys]
     kidx = {n: i for i, n in enumerate(names)}
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -298,7 +301,7 @@ def fit_fast(args):
     for n in names:
         r = ini["rungs"].get(n)
         if r is None:      # new rung: start from its unicast sibling, else a generic guess
-            base = n.replace("_mc2_", "_").replace("_mc4_", "_")
+            base = n.replace("_mc2_", "_").replace("_mc4_", "_").replace("_o2_", "_")
             r = ini["rungs"].get(base, {"mac_milli": 2048000, "l2s_milli": 96000,
                                         "epi_milli": 64000, "fixed": 3000})
         x += [math.log(r["mac_milli"] / 1000), math.log(r["l2s_milli"] / 1000),
@@ -316,7 +319,8 @@ def fit_fast(args):
     lo += [math.log(2), math.log(1), math.log(1)]
     hi += [math.log(64), math.log(8000), math.log(256)]
     x = [min(max(v, a), b) for v, a, b in zip(x, lo, hi)]
-    samp_key = [kidx[calib_key(fam[sm["family"]], sm["bm"], sm["bn"], sm.get("mc", 1))] for sm in S]
+    samp_key = [kidx[calib_key(fam[sm["family"]], sm["bm"], sm["bn"], sm.get("mc", 1), sm.get("occ", 1))]
+                for sm in S]
     by_rung = {}
     for j, kk in enumerate(samp_key):
         by_rung.setdefault(kk, []).append(j)
@@ -431,9 +435,9 @@ def heldout(args):
             def pred(f):
                 r = rt[f["rung"]]
                 sm = dict(M=M, N=N, K=K, split=f["split"], family=r["family"], bm=r["bm"], bn=r["bn"],
-                          mc=r.get("mc", 1))
-                return model_us(sm, th[calib_key(fam[r["family"]], r["bm"], r["bn"], r.get("mc", 1))],
-                                desc, g)
+                          mc=r.get("mc", 1), occ=r.get("occ", 1))
+                return model_us(sm, th[calib_key(fam[r["family"]], r["bm"], r["bn"], r.get("mc", 1),
+                                                 r.get("occ", 1))], desc, g)
             pick = min(e["forced"], key=pred)
             regs.append(best / pick["us"])
             tag = "bert" if K == 768 else "llama"
