@@ -173,7 +173,7 @@ vx_status vx_calibrate(int device, vx_blayout bl, int32_t effort, vx_calib_t* ou
  * vx_calib_set_rung per rung key ("umma_128x128", "umma_swap_mc2_128x64", "gemv_4x8", ...;
  * the keys vx_plan_dump reports through its rung fields). */
 vx_status vx_calib_new(int64_t hbm_milli, int64_t dsm_milli, int64_t fixed_cluster,
-                       int64_t skfix_milli, vx_calib_t* out);
+                       int64_t skfix_milli, int64_t stagger, vx_calib_t* out);
 vx_status vx_calib_set_rung(vx_calib_t calib, const char* key, int64_t mac_milli,
                             int64_t l2s_milli, int64_t epi_milli, int64_t fixed);
 vx_status vx_calib_destroy(vx_calib_t calib);

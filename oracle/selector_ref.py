@@ -146,8 +146,9 @@ IMPL_TC = {(0, 128, 64), (0, 128, 128), (0, 128, 192), (0, 128, 256), (0, 256, 6
            (1, 128, 192), (1, 128, 256)}
 # TMA-multicast cluster kernels: (family, bm, bn, mc), mc CTAs sharing the A tile
 IMPL_MC = {(0, 128, 128, 2), (0, 128, 256, 2), (1, 128, 32, 2), (1, 128, 64, 2), (1, 128, 64, 4)}
-# occupancy-2 (lean) kernels: (family, bm, bn), two CTAs per SM (R5b)
-IMPL_LEAN = {(0, 128, 64), (1, 128, 32), (1, 128, 64)}
+# occupancy-2 (lean) kernels: (family, bm, bn), two CTAs per SM (R5b) -- none instantiated
+# (measured slower); the L2 candidates remain in the level counts
+IMPL_LEAN = set()
 MC_SIZES = (1, 2, 4)
 SIMT_TILES = ((32, 32, 2, 4), (64, 64, 4, 4), (128, 64, 8, 4))
 SIMT_BK = 16
@@ -379,6 +380,10 @@ def rung_cost(rung: dict, s: int, batch: int, M: int, N: int, K: int,
         cost = temporal_cost(tmain, F, ts, 0) + cal["fixed"]
     else:
         cost = level_cost(F, T) + cal["fixed"] + (calib["fixed_cluster"] if s > 1 else 0)
+    # R21: back to back, a first wave of more than half the SMs cannot become resident
+    # while the previous grid (one full-SMEM CTA per SM) still holds its SMs
+    if rung["family"] != 2 and min(W, slots) > desc["sm_count"] // 2:
+        cost += calib["stagger"]
     return {"cost": cost, "tiles_m": tm, "tiles_n": tn, "tiles": tiles, "F": F,
             "grid": W if s > 1 or rung["family"] == 2 else min(W, slots),
             "padded_work": batch * tm_c * bm * tn_c * bn}
@@ -424,6 +429,8 @@ def _streamk_cost(rung, batch, M, N, K, mt, nt, tm, tn, tiles, kb, in_b, out_b, 
     st = max(t_load(bm * bn * out_b, cal["epi_milli"]), t_load(out_b * batch * M * N, segs * hbm))
     fix = ceil_div(kb, units) * t_load(2 * bm * bn * 4, calib["skfix_milli"])
     cost = max(t_main, segs * st) + st + fix + cal["fixed"]
+    if G * cg > desc["sm_count"] // 2:               # R21 (see rung_cost)
+        cost += calib["stagger"]
     return {"cost": cost, "tiles_m": tm, "tiles_n": tn, "tiles": tiles, "F": 1, "grid": G * cg,
             "padded_work": batch * tm * bm * tn * bn}
 

@@ -97,7 +97,7 @@ def _load():
     L.vx_gemm_gather.argtypes = [P, i64, i64, i64, vp, vp, i32, ctypes.POINTER(vp), i64, i32,
                                  i32, vp, ctypes.POINTER(Choice)]
     L.vx_calibrate.argtypes = [ctypes.c_int, ctypes.c_int, i32, ctypes.POINTER(P)]
-    L.vx_calib_new.argtypes = [i64, i64, i64, i64, ctypes.POINTER(P)]
+    L.vx_calib_new.argtypes = [i64, i64, i64, i64, i64, ctypes.POINTER(P)]
     L.vx_calib_set_rung.argtypes = [P, ctypes.c_char_p, i64, i64, i64, i64]
     L.vx_calib_destroy.argtypes = [P]
     L.vx_calib_dump.argtypes = [P, ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]
@@ -163,7 +163,7 @@ class Calib:
     def from_dict(cls, d: dict) -> "Calib":
         h = ctypes.c_void_p()
         _check(_lib.vx_calib_new(d["hbm_milli"], d["dsm_milli"], d["fixed_cluster"],
-                                 d["skfix_milli"], ctypes.byref(h)), "vx_calib_new")
+                                 d["skfix_milli"], d["stagger"], ctypes.byref(h)), "vx_calib_new")
         c = cls(h)
         for k, r in d["rungs"].items():
             _check(_lib.vx_calib_set_rung(h, k.encode(), r["mac_milli"], r["l2s_milli"],

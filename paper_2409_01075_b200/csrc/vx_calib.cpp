@@ -26,6 +26,7 @@ static const Calib kCalib = {
     /*dsm_milli=*/2931,      // effective in-cluster reduce rate (fitted)
     /*fixed_cluster=*/2538,  // cluster launch + two cluster barriers (fitted)
     /*skfix_milli=*/13315,   // stream-K partial write + read-back (fitted)
+    /*stagger=*/4000,       // first wave > sm_count / 2 CTAs, back to back (R21; fitted)
 };
 
 static const RungCalib kRungs[] = {
@@ -43,10 +44,6 @@ static const RungCalib kRungs[] = {
     {"umma_128x192", 1470000, 106501, 34060, 200},
     {"umma_swap_128x192", 1738143, 100193, 33920, 450},
     {"umma_swap_128x256", 1936545, 160000, 29217, 450},
-    // occupancy-2 (lean) CTAs (R5b): provisional = the occupancy-1 rung's constants
-    {"umma_o2_128x64", 1000367, 46224, 8000, 3658},
-    {"umma_swap_o2_128x32", 1000000, 28993, 8000, 4315},
-    {"umma_swap_o2_128x64", 1000000, 49863, 90313, 4743},
     // TMA-multicast clusters
     {"umma_mc2_128x128", 1744850, 41151, 13097, 2547},
     {"umma_mc2_128x256", 4096000, 38348, 512000, 3025},

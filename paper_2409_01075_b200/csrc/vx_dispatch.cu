@@ -38,10 +38,13 @@ static bool mc_available(int family, int bm, int bn, int mc) {
     return false;
 }
 
-// occupancy-2 (lean) rungs: 128 x 64 non-swapped, swapped 128 x {32, 64}
+// occupancy-2 (lean) rungs: the kernel exists (vx_umma_kernel<..., LEAN = true>) and was
+// measured integer-exact, but slower than the occupancy-1 rungs on every BERT-size shape
+// tried (its <= ~110 KB ring keeps too few bytes in flight: 8.3 vs 6.2 us at M=128,
+// N=3072, K=768), so no lean rung is instantiated.  The strategy table keeps
+// the occupancy-2 L2 candidates (R5b); they are filtered here as unimplemented (R6).
 static bool lean_available(int family, int bm, int bn) {
-    if (family == kUmma) return bm == 128 && bn == 64;
-    if (family == kUmmaSwap) return bm == 128 && (bn == 32 || bn == 64);
+    (void)family; (void)bm; (void)bn;
     return false;
 }
 
@@ -84,19 +87,11 @@ static UmmaFn pick_mc(bool b_mn) {
                 : (UmmaFn)vx_umma_kernel<BN, false, false, false, false, MC>;
 }
 
-template <int BN, bool SWAP>
-static UmmaFn pick_lean(bool b_mn) {
-    if (SWAP) return b_mn ? (UmmaFn)vx_umma_kernel<BN, true, true, false, false, 1, true>
-                          : (UmmaFn)vx_umma_kernel<BN, true, false, false, false, 1, true>;
-    return b_mn ? (UmmaFn)vx_umma_kernel<BN, false, false, true, false, 1, true>
-                : (UmmaFn)vx_umma_kernel<BN, false, false, false, false, 1, true>;
-}
 
 static UmmaFn umma_fn(int family, int bm, int bn, bool b_mn, int mc = 1, int occ = 1) {
     if (occ == 2) {
         if (mc != 1 || !lean_available(family, bm, bn)) return nullptr;
-        if (family == kUmma) return pick_lean<64, false>(b_mn);
-        return bn == 32 ? pick_lean<32, true>(b_mn) : pick_lean<64, true>(b_mn);
+        return nullptr;   // no lean kernel instantiated (see lean_available)
     }
     if (mc > 1) {
         if (!mc_available(family, bm, bn, mc)) return nullptr;

@@ -48,6 +48,9 @@ struct Rung {
 
 struct Calib {
     int64_t hbm_milli, dsm_milli, fixed_cluster, skfix_milli;
+    int64_t stagger;   // cycles a tcgen05 launch loses when its first wave needs more than
+                       // half the SMs: back to back, its CTAs cannot all become resident
+                       // while the previous grid still holds its SMs (R21)
 };
 
 struct RungCalib {

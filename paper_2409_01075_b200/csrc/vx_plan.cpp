@@ -308,6 +308,7 @@ static void rung_cost(const vx_plan_s* p, const Rung& r, int s, int64_t batch, i
         o->tiles_m = (int32_t)tm; o->tiles_n = (int32_t)tn; o->grid = (int32_t)(G * r.cg);
         o->cluster = r.cg; o->mc = 1;
         o->cost = std::max(tm_, segs * st) + st + fix + r.fixed;
+        if (G * r.cg > d.sm_count / 2) o->cost += cal.stagger;   // R21
         return;
     }
     const int64_t trips = kb / s;            // sizeof(TemporalLoop) at the CTA level (R8)
@@ -370,6 +371,9 @@ static void rung_cost(const vx_plan_s* p, const Rung& r, int s, int64_t batch, i
     o->grid = (int32_t)((s > 1 || r.family == kSimt) ? W : std::min(W, slots));
     o->cluster = (int32_t)(s * r.cg * mc);
     o->mc = (int32_t)mc;
+    // R21: back to back, a first wave wider than half the SMs cannot become resident while
+    // the previous grid holds its SMs (one full-SMEM CTA per SM)
+    if (r.family != kSimt && std::min(W, slots) > d.sm_count / 2) cost += cal.stagger;
     o->cost = cost;
 }
 
@@ -538,14 +542,14 @@ vx_status vx_plan_calibrated(int64_t N, int64_t K, vx_dtype in, vx_dtype out, vx
 }
 
 vx_status vx_calib_new(int64_t hbm_milli, int64_t dsm_milli, int64_t fixed_cluster,
-                       int64_t skfix_milli, vx_calib_t* out) {
+                       int64_t skfix_milli, int64_t stagger, vx_calib_t* out) {
     if (!out) { set_error("NULL argument"); return VX_ERR_INVALID; }
-    if (hbm_milli <= 0 || dsm_milli <= 0 || fixed_cluster < 0 || skfix_milli <= 0) {
+    if (hbm_milli <= 0 || dsm_milli <= 0 || fixed_cluster < 0 || skfix_milli <= 0 || stagger < 0) {
         set_error("calibration rates must be > 0"); return VX_ERR_INVALID;
     }
     vx_calib_s* c = new (std::nothrow) vx_calib_s();
     if (!c) return VX_ERR_OOM;
-    c->table.glob = {hbm_milli, dsm_milli, fixed_cluster, skfix_milli};
+    c->table.glob = {hbm_milli, dsm_milli, fixed_cluster, skfix_milli, stagger};
     c->table.source = "user";
     *out = c;
     return VX_OK;
@@ -573,9 +577,10 @@ vx_status vx_calib_dump(vx_calib_t c, char* buf, size_t cap, size_t* need) {
     std::string s;
     char tmp[256];
     snprintf(tmp, sizeof tmp, "{\"source\":\"%s\",\"hbm_milli\":%lld,\"dsm_milli\":%lld,"
-             "\"fixed_cluster\":%lld,\"skfix_milli\":%lld,\"rungs\":{", t.source.c_str(),
-             (long long)t.glob.hbm_milli, (long long)t.glob.dsm_milli,
-             (long long)t.glob.fixed_cluster, (long long)t.glob.skfix_milli);
+             "\"fixed_cluster\":%lld,\"skfix_milli\":%lld,\"stagger\":%lld,\"rungs\":{",
+             t.source.c_str(), (long long)t.glob.hbm_milli, (long long)t.glob.dsm_milli,
+             (long long)t.glob.fixed_cluster, (long long)t.glob.skfix_milli,
+             (long long)t.glob.stagger);
     s += tmp;
     for (size_t i = 0; i < t.rungs.size(); ++i) {
         const RungConst& r = t.rungs[i];
@@ -627,11 +632,12 @@ vx_status vx_plan_dump(vx_plan_t p, char* buf, size_t cap, size_t* need) {
     snprintf(tmp, sizeof tmp,
              "{\"abi\":%d,\"N\":%lld,\"K\":%lld,\"in\":\"%s\",\"out\":\"%s\",\"b_layout\":\"%s\","
              "\"levels\":{\"l0\":%lld,\"l1\":%lld,\"l2\":%lld,\"l3\":%lld},"
-             "\"calib\":{\"hbm_milli\":%lld,\"dsm_milli\":%lld,\"fixed_cluster\":%lld,\"skfix_milli\":%lld},\"rungs\":[",
+             "\"calib\":{\"hbm_milli\":%lld,\"dsm_milli\":%lld,\"fixed_cluster\":%lld,\"skfix_milli\":%lld,\"stagger\":%lld},\"rungs\":[",
              VX_ABI_VERSION, (long long)p->N, (long long)p->K, dt_name(p->in), dt_name(p->out),
              p->bl == VX_B_KN ? "kn" : p->bl == VX_B_NK ? "nk" : "packed", (long long)p->counts.l0, (long long)p->counts.l1,
              (long long)p->counts.l2, (long long)p->counts.l3, (long long)c.hbm_milli,
-             (long long)c.dsm_milli, (long long)c.fixed_cluster, (long long)c.skfix_milli);
+             (long long)c.dsm_milli, (long long)c.fixed_cluster, (long long)c.skfix_milli,
+             (long long)c.stagger);
     s += tmp;
     for (size_t i = 0; i < p->rungs.size(); ++i) {
         const Rung& r = p->rungs[i];

@@ -29,8 +29,9 @@ def _rung(d):
 
 @pytest.mark.parametrize("case", CV["rung_cost"], ids=[c["name"] for c in CV["rung_cost"]])
 def test_rung_cost_worked_examples(case):
+    cal = dict(CV["calib"], **case.get("calib_override", {}))
     c = S.rung_cost(_rung(case["rung"]), case["split"], case["batch"], case["M"], case["N"],
-                    case["K"], "bf16", "bf16", CV["desc"], CV["calib"])
+                    case["K"], "bf16", "bf16", CV["desc"], cal)
     for k, v in case["want"].items():
         assert c[k] == v, (case["name"], k, c[k], v)
 

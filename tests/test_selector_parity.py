@@ -48,7 +48,7 @@ def test_tables_identical(K, io):
 def test_calibration_copies_agree():
     d = vx.Plan(4096, 4096, "bf16", "bf16", "nk", desc=DESC).dump()
     assert d["calib"] == {k: CAL[k] for k in ("hbm_milli", "dsm_milli", "fixed_cluster",
-                                              "skfix_milli")}
+                                              "skfix_milli", "stagger")}
     for r in d["rungs"]:
         key = S._calib_key(r)
         for f in ("mac_milli", "l2s_milli", "epi_milli", "fixed"):
@@ -115,7 +115,7 @@ def test_builtin_calibration_dump_matches_oracle_copy():
     """vx_calib_dump(NULL) is the compiled-in empirical tier; the oracle's JSON copy agrees."""
     d = vx.builtin_calib()
     assert d["source"] == "compiled-in"
-    for k in ("hbm_milli", "dsm_milli", "fixed_cluster", "skfix_milli"):
+    for k in ("hbm_milli", "dsm_milli", "fixed_cluster", "skfix_milli", "stagger"):
         assert d[k] == CAL[k]
     for key, r in CAL["rungs"].items():
         assert d["rungs"][key] == r, key
@@ -130,7 +130,7 @@ def test_selection_parity_under_arbitrary_calibration(seed):
     import random
     rnd = random.Random(seed)
     cal = json.loads(json.dumps(CAL))
-    for k in ("dsm_milli", "fixed_cluster", "skfix_milli"):
+    for k in ("dsm_milli", "fixed_cluster", "skfix_milli", "stagger"):
         cal[k] = max(1, int(cal[k] * rnd.uniform(0.5, 2.0)))
     for r in cal["rungs"].values():
         for f in ("mac_milli", "l2s_milli", "epi_milli", "fixed"):
@@ -140,7 +140,7 @@ def test_selection_parity_under_arbitrary_calibration(seed):
         p = vx.Plan(N, K, "bf16", "bf16", "nk", desc=DESC, calib=c)
         d = p.dump()
         assert d["calib"] == {k: cal[k] for k in ("hbm_milli", "dsm_milli", "fixed_cluster",
-                                                  "skfix_milli")}
+                                                  "skfix_milli", "stagger")}
         t = _oracle_table(K, "bf16", "bf16")
         for M in list(range(1, 600, 7)) + [1023, 1024, 4097, 16383]:
             got = p.select(M)

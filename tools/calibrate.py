@@ -122,6 +122,8 @@ def model_us(sm, th, desc, g):
         tm_ = l + (units - 1) * max(l, c) + c
         st = max(t(bm * bn * 2, epi), t(2 * M * N, segs * hbm))
         cyc = max(tm_, segs * st) + st + _cd(kb, units) * t(2 * bm * bn * 4, skfix) + fixed
+        if G * cgk > desc["sm_count"] // 2:          # R21
+            cyc += int(round(g.get("stagger", 0)))
         return cyc / (CLOCK_GHZ * 1e3)
     cg = 2 if bm == 256 else 1
     trips = kb // s
@@ -140,6 +142,8 @@ def model_us(sm, th, desc, g):
         cyc = tmain + (F - 1) * max(tmain, st) + st + fixed
     else:
         cyc = F * T + fixed + fixed_cluster
+    if min(W, slots) > desc["sm_count"] // 2:        # R21
+        cyc += int(round(g.get("stagger", 0)))
     return cyc / (CLOCK_GHZ * 1e3)
 
 
@@ -307,7 +311,7 @@ def fit_fast(args):
         x += [math.log(r["mac_milli"] / 1000), math.log(r["l2s_milli"] / 1000),
               math.log(r["epi_milli"] / 1000), math.log(max(r["fixed"], 1))]
     x += [math.log(ini.get("dsm_milli", 20000) / 1000), math.log(max(ini.get("fixed_cluster", 1500), 1)),
-          math.log(ini.get("skfix_milli", 32000) / 1000)]
+          math.log(ini.get("skfix_milli", 32000) / 1000), math.log(max(ini.get("stagger", 4000), 1))]
     lo, hi = [], []
     for k in keys:
         if k[0] == "gemv":
@@ -316,8 +320,8 @@ def fit_fast(args):
         else:
             lo += [math.log(1000), math.log(8), math.log(8), math.log(200)]
             hi += [math.log(4096), math.log(160), math.log(512), math.log(12000)]
-    lo += [math.log(2), math.log(1), math.log(1)]
-    hi += [math.log(64), math.log(8000), math.log(256)]
+    lo += [math.log(2), math.log(1), math.log(1), math.log(1)]
+    hi += [math.log(64), math.log(8000), math.log(256), math.log(20000)]
     x = [min(max(v, a), b) for v, a, b in zip(x, lo, hi)]
     samp_key = [kidx[calib_key(fam[sm["family"]], sm["bm"], sm["bn"], sm.get("mc", 1), sm.get("occ", 1))]
                 for sm in S]
@@ -341,7 +345,8 @@ def fit_fast(args):
                     epi=math.exp(x[4 * i + 2]), fixed=math.exp(x[4 * i + 3]))
 
     def g_of(x):
-        return dict(hbm=hbm, dsm=math.exp(x[-3]), fixed_cluster=math.exp(x[-2]), skfix=math.exp(x[-1]))
+        return dict(hbm=hbm, dsm=math.exp(x[-4]), fixed_cluster=math.exp(x[-3]),
+                    skfix=math.exp(x[-2]), stagger=math.exp(x[-1]))
 
     pred = np.zeros(len(S))
 
@@ -396,7 +401,8 @@ def fit_fast(args):
     g = g_of(x)
     out = {"hbm_milli": int(round(hbm * 1000)), "dsm_milli": int(round(g["dsm"] * 1000)),
            "fixed_cluster": int(round(g["fixed_cluster"])),
-           "skfix_milli": int(round(g["skfix"] * 1000)), "rungs": {}}
+           "skfix_milli": int(round(g["skfix"] * 1000)), "stagger": int(round(g["stagger"])),
+           "rungs": {}}
     for i, n in enumerate(names):
         t = th_of(x, i)
         out["rungs"][n] = {"mac_milli": int(round(t["mac"] * 1000)),
@@ -422,7 +428,8 @@ def heldout(args):
         th = {n: dict(mac=r["mac_milli"] / 1000, l2s=r["l2s_milli"] / 1000, epi=r["epi_milli"] / 1000,
                       fixed=r["fixed"]) for n, r in cal["rungs"].items()}
         g = dict(hbm=cal["hbm_milli"] / 1000, dsm=cal["dsm_milli"] / 1000,
-                 fixed_cluster=cal["fixed_cluster"], skfix=cal["skfix_milli"] / 1000)
+                 fixed_cluster=cal["fixed_cluster"], skfix=cal["skfix_milli"] / 1000,
+                 stagger=cal.get("stagger", 0))
         plans, regs, by = {}, [], {}
         for e in sw:
             if e.get("batch", 1) != 1:

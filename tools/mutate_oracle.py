@@ -65,6 +65,15 @@ MUTATIONS = [
     ("rung_cost", "multicast clusters use the single-CTA residency",
      "        csz = s * rung[\"cg\"] * mc                     # CTAs per cluster",
      "        csz = s * rung[\"cg\"]                          # CTAs per cluster"),
+    ("rung_cost", "stagger (R21) charged whatever the first-wave width",
+     "    if rung[\"family\"] != 2 and min(W, slots) > desc[\"sm_count\"] // 2:",
+     "    if rung[\"family\"] != 2:"),
+    ("rung_cost", "stagger (R21) threshold at all SMs instead of half",
+     "    if rung[\"family\"] != 2 and min(W, slots) > desc[\"sm_count\"] // 2:",
+     "    if rung[\"family\"] != 2 and min(W, slots) > desc[\"sm_count\"]:"),
+    ("_streamk_cost", "stream-K launches never charged the stagger (R21)",
+     "    if G * cg > desc[\"sm_count\"] // 2:               # R21 (see rung_cost)",
+     "    if False:"),
     ("_streamk_cost", "segment count without the +1 boundary segment",
      "    segs = ceil_div(units, kb) + 1", "    segs = ceil_div(units, kb)"),
     ("_streamk_cost", "fix-up partial count floored",
