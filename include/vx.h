@@ -195,6 +195,11 @@ vx_status vx_plan_ex_calibrated(int64_t N, int64_t K, vx_dtype in, vx_dtype out,
  * (pass it anyway).  batch >= 1, M >= 1, N >= 1. */
 vx_status vx_plan_select(vx_plan_t plan, int64_t batch, int64_t M, int64_t N, vx_choice* out);
 
+/* Runtime selection for a ragged batch (host, pure): the decision vx_gemm_varlen makes for
+ * sequence offsets cu[0..ngroups] (cu[0] = 0, non-decreasing). */
+vx_status vx_plan_select_varlen(vx_plan_t plan, int32_t ngroups, const int32_t* cu,
+                                vx_choice* out);
+
 /* Cost of one forced (rung, split) for the shape (same model vx_plan_select minimises);
  * VX_ERR_INVALID if the pair is not in the table. */
 vx_status vx_plan_cost(vx_plan_t plan, int32_t rung_id, int32_t split, int64_t batch,
@@ -238,6 +243,18 @@ vx_status vx_gemm_ex(vx_plan_t plan, int64_t batch, int64_t M, int64_t N, int64_
 vx_status vx_gemm_gather(vx_plan_t plan, int64_t M, int64_t N, int64_t K, const void* A,
                          const void* B, int32_t ndst, void* const* dst, int64_t row_offset,
                          int32_t force_rung, int32_t force_split, void* stream, vx_choice* used);
+
+/* Ragged attention batch (the varlen reading of BASELINE config 4):
+ * S_g = Q_g x K_g^T for g < ngroups sequences of lengths s_g = cu[g+1] - cu[g], in ONE
+ * launch.  Q and Kt are packed row-major [cu[ngroups], K] (sequence g in rows [cu[g],
+ * cu[g+1])), Kt being K stored N x K; S is packed: S_g is s_g x s_g row-major at element
+ * offset sum_{j<g} s_j^2.  The plan must have N = 0 (dynamic), 16-bit inputs and
+ * VX_B_NK.  cu_host is read on the host (selection: Eqs. 2-4 over the ragged tile set,
+ * grid); cu_dev (same ngroups + 1 int32 values, device) is read by the kernel.
+ * force_rung < 0 selects; used (optional) receives the decision (tiles_m = tiles_n = 0). */
+vx_status vx_gemm_varlen(vx_plan_t plan, int32_t ngroups, const int32_t* cu_host,
+                         const int32_t* cu_dev, int64_t K, const void* Q, const void* Kt, void* S,
+                         int32_t force_rung, void* stream, vx_choice* used);
 
 /* Host-staged form (the e2e measurement): A, B, C are HOST pointers (pinned for full
  * speed); dA, dB, dC are caller-owned device buffers of the same sizes.  Enqueues

@@ -435,6 +435,52 @@ def _streamk_cost(rung, batch, M, N, K, mt, nt, tm, tn, tiles, kb, in_b, out_b, 
             "padded_work": batch * tm * bm * tn * bn}
 
 
+def varlen_cost(rung: dict, lens, K: int, in_dtype: str, out_dtype: str, desc: dict,
+                calib: dict) -> dict:
+    """Ragged attention batch: S_g = Q_g K_g^T for sequence lengths `lens`.
+    Eqs. 2-4 over the ragged tile set: W = sum_g ceil(s_g/BM) ceil(s_g/BN) (padding only at
+    each sequence's edge), unique operand bytes in_b K 2 sum_g s_g, output bytes out_b
+    sum_g s_g^2, the persistent grid-level Eq. 2 (R11) and the stagger (R21)."""
+    in_b, out_b = IN_BYTES[in_dtype], OUT_BYTES[out_dtype]
+    cal = _calib_for(rung, calib)
+    hbm = calib["hbm_milli"]
+    bm, bn, bk = rung["bm"], rung["bn"], rung["bk"]
+    tiles = sum(ceil_div(s, bm) * ceil_div(s, bn) for s in lens)
+    rows = sum(lens)
+    outs = sum(s * s for s in lens)
+    padded = sum(ceil_div(s, bm) * bm * ceil_div(s, bn) * bn for s in lens)
+    kb = ceil_div(K, bk)
+    slots = desc["max_active_clusters"]["1"]
+    W = max(tiles, 1)
+    F = parallel_factor(W, slots)
+    inner = t_load(bm * bn * bk, cal["mac_milli"])
+    l_smem = t_load((bm + bn) * bk * in_b, cal["l2s_milli"])
+    l_hbm = t_load(in_b * K * 2 * rows, F * kb * hbm)
+    tl = max(l_smem, l_hbm)
+    ts = max(t_load(bm * bn * out_b, cal["epi_milli"]), t_load(out_b * outs, F * hbm))
+    T = temporal_cost(tl, kb, inner, ts)
+    cost = temporal_cost(T - ts, F, ts, 0) + cal["fixed"]
+    if min(W, slots) > desc["sm_count"] // 2:
+        cost += calib["stagger"]
+    return {"cost": cost, "tiles": tiles, "grid": min(W, slots), "padded_work": padded, "F": F}
+
+
+def select_varlen(table: dict, lens, K: int, desc: dict, calib: dict) -> dict:
+    """Eq. 1 over the non-swapped cta_group::1 persistent tcgen05 rungs for a ragged batch;
+    key (cost, padded_work, rung_id)."""
+    best = None
+    for r in table["rungs"]:
+        if r["family"] != 0 or r["cg"] != 1 or r["mc"] != 1 or r["occ"] != 1:
+            continue
+        c = varlen_cost(r, lens, K, table["in"], table["out"], desc, calib)
+        key = (c["cost"], c["padded_work"], r["rung_id"])
+        if best is None or key < best[0]:
+            best = (key, r, c)
+    key, r, c = best
+    return {"rung_id": r["rung_id"], "split": 1, "grid": c["grid"], "cost": c["cost"],
+            "bm": r["bm"], "bn": r["bn"]}
+
+
 SK_MAX_WAVES = 3
 
 

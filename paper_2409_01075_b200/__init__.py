@@ -97,6 +97,9 @@ def _load():
     L.vx_gemm_gather.argtypes = [P, i64, i64, i64, vp, vp, i32, ctypes.POINTER(vp), i64, i32,
                                  i32, vp, ctypes.POINTER(Choice)]
     L.vx_calibrate.argtypes = [ctypes.c_int, ctypes.c_int, i32, ctypes.POINTER(P)]
+    L.vx_gemm_varlen.argtypes = [P, i32, ctypes.POINTER(i32), vp, i64, vp, vp, vp, i32, vp,
+                                 ctypes.POINTER(Choice)]
+    L.vx_plan_select_varlen.argtypes = [P, i32, ctypes.POINTER(i32), ctypes.POINTER(Choice)]
     L.vx_calib_new.argtypes = [i64, i64, i64, i64, i64, ctypes.POINTER(P)]
     L.vx_calib_set_rung.argtypes = [P, ctypes.c_char_p, i64, i64, i64, i64]
     L.vx_calib_destroy.argtypes = [P]
@@ -114,7 +117,7 @@ def _load():
               "vx_plan_cost", "vx_plan_dump", "vx_gemm", "vx_gemm_batched", "vx_gemm_ex",
               "vx_gemm_host", "vx_gemm_gather", "vx_calibrate", "vx_calib_new",
               "vx_calib_set_rung", "vx_calib_destroy", "vx_calib_dump", "vx_plan_calibrated",
-              "vx_plan_ex_calibrated"):
+              "vx_plan_ex_calibrated", "vx_gemm_varlen", "vx_plan_select_varlen"):
         getattr(L, f).restype = ctypes.c_int
     if L.vx_abi_version() != 1:
         raise ImportError("libvx.so ABI %d != binding ABI 1 (rebuild)" % L.vx_abi_version())
@@ -245,6 +248,13 @@ class Plan:
                                    ctypes.byref(c)), "vx_plan_select")
         return c.as_dict()
 
+    def select_varlen(self, cu_seqlens) -> dict:
+        cu = [int(x) for x in cu_seqlens]
+        c = Choice()
+        _check(_lib.vx_plan_select_varlen(self._h, len(cu) - 1, (ctypes.c_int32 * len(cu))(*cu),
+                                          ctypes.byref(c)), "vx_plan_select_varlen")
+        return c.as_dict()
+
     def cost(self, rung_id: int, split: int, M: int, N: int | None = None, batch: int = 1) -> dict:
         c = Choice()
         _check(_lib.vx_plan_cost(self._h, rung_id, split, batch, M, self.N if N is None else N,
@@ -355,6 +365,34 @@ class Plan:
                                    row_offset, fr, fs, _stream_ptr(stream), ctypes.byref(ch)),
                "vx_gemm_gather")
         return ch.as_dict() if want_choice else None
+
+    def gemm_varlen(self, Q, Kt, cu_seqlens, out=None, stream=None, force: int = -1,
+                    want_choice: bool = False):
+        """Ragged attention batch (vx_gemm_varlen): S_g = Q_g K_g^T for packed Q, Kt
+        [total, d] and cu_seqlens (list/tensor of ngroups + 1 offsets).  Returns the packed
+        S (sum_g s_g^2 elements)."""
+        import torch
+        cu = [int(x) for x in (cu_seqlens.tolist() if hasattr(cu_seqlens, "tolist") else cu_seqlens)]
+        ng = len(cu) - 1
+        for t, nm in ((Q, "Q"), (Kt, "Kt")):
+            if not t.is_cuda or not t.is_contiguous() or _dt_name(t) != self.in_dtype:
+                raise ValueError("%s must be a contiguous CUDA %s tensor" % (nm, self.in_dtype))
+        if Q.shape != Kt.shape or Q.shape[0] != cu[-1] or Q.shape[1] != self.K:
+            raise ValueError("Q and Kt must be [cu[-1], K]")
+        odt = {"bf16": torch.bfloat16, "fp16": torch.float16, "fp32": torch.float32}[self.out_dtype]
+        n_out = sum((cu[g + 1] - cu[g]) ** 2 for g in range(ng))
+        if out is None:
+            out = torch.empty(n_out, dtype=odt, device=Q.device)
+        elif out.numel() < n_out or out.dtype != odt or not out.is_contiguous():
+            raise ValueError("out must hold %d contiguous %s elements" % (n_out, odt))
+        cu_h = (ctypes.c_int32 * len(cu))(*cu)
+        cu_d = torch.tensor(cu, dtype=torch.int32, device=Q.device)
+        self._cu_keep = cu_d          # keep alive until the launch has consumed it
+        ch = Choice()
+        _check(_lib.vx_gemm_varlen(self._h, ng, cu_h, cu_d.data_ptr(), self.K, Q.data_ptr(),
+                                   Kt.data_ptr(), out.data_ptr(), force, _stream_ptr(stream),
+                                   ctypes.byref(ch)), "vx_gemm_varlen")
+        return (out, ch.as_dict()) if want_choice else out
 
     def gemm_host(self, batch, M, N, K, hA, hB, hC, dA, dB, dC, stream_ptr):
         _check(_lib.vx_gemm_host(self._h, batch, M, N, K, hA, hB, hC, dA, dB, dC, stream_ptr),

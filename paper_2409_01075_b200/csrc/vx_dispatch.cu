@@ -342,7 +342,7 @@ static vx_status ensure_ws(const vx_plan_s* pc, void* stream, void** out) {
 
 vx_status launch(const vx_plan_s* p, const vx_choice& ch, int64_t batch, int64_t M, int64_t N,
                  int64_t K, const void* A, int64_t sA, const void* B, int64_t sB, void* C,
-                 int64_t sC, void* stream, const GatherSpec* gather) {
+                 int64_t sC, void* stream, const GatherSpec* gather, const VarSpec* var) {
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     const vx::Rung& r = p->rungs[ch.rung_id];
     if (r.family == kSimt) {
@@ -500,6 +500,16 @@ vx_status launch(const vx_plan_s* p, const vx_choice& ch, int64_t batch, int64_t
     prm.ndst = 0;
     prm.dst_row0 = 0;
     for (int d = 0; d < 8; ++d) prm.dst[d] = nullptr;
+    prm.cu = nullptr;
+    prm.ngroups = 0;
+    if (var) {
+        // ragged batch: tiles enumerate every sequence's (tp, tq); each sequence's S block
+        // is stored from registers (no C tensor map), vectorised per sequence when aligned
+        prm.cu = var->cu_dev;
+        prm.ngroups = var->ngroups;
+        prm.num_tiles = (int)var->tiles;
+        prm.vec = 0;
+    }
     if (gather) {
         // fused all-gather epilogue: vector stores iff every destination
         // row is 16-B aligned
@@ -730,6 +740,43 @@ vx_status vx_gemm_gather(vx_plan_t p, int64_t M, int64_t N, int64_t K, const voi
     g.row0 = row_offset;
     for (int d = 0; d < 8; ++d) g.dst[d] = d < ndst ? dst[d] : nullptr;
     return launch(p, ch, 1, M, N, K, A, M * K, B, N * K, dst[0], M * N, stream, &g);
+}
+
+vx_status vx_gemm_varlen(vx_plan_t p, int32_t ngroups, const int32_t* cu_host,
+                         const int32_t* cu_dev, int64_t K, const void* Q, const void* Kt, void* S,
+                         int32_t force_rung, void* stream, vx_choice* used) {
+    if (!p || !cu_host || !cu_dev || !Q || !Kt || !S || ngroups < 1) {
+        set_error("varlen: NULL argument or ngroups < 1"); return VX_ERR_INVALID;
+    }
+    if (p->N != 0 || p->in == VX_FP32 || p->bl != VX_B_NK) {
+        set_error("varlen needs a dynamic-N (N = 0) 16-bit plan with B stored N x K (K^T rows)");
+        return VX_ERR_UNSUPPORTED;
+    }
+    if (K != p->K) { set_error("K=%lld does not match the plan's K=%lld", (long long)K, (long long)p->K); return VX_ERR_INVALID; }
+    if (cu_host[0] != 0) { set_error("cu_seqlens[0] must be 0"); return VX_ERR_INVALID; }
+    for (int32_t g = 0; g < ngroups; ++g)
+        if (cu_host[g + 1] < cu_host[g]) { set_error("cu_seqlens must be non-decreasing"); return VX_ERR_INVALID; }
+    const int64_t total = cu_host[ngroups];
+    if (total == 0) return VX_OK;
+    if (K % 8 || !aligned16(Q) || !aligned16(Kt)) { set_error("varlen: K %% 8 and 16-B aligned Q, K^T"); return VX_ERR_ALIGN; }
+    if (reinterpret_cast<uintptr_t>(S) % out_bytes(p->out)) { set_error("S must be element aligned"); return VX_ERR_ALIGN; }
+    if (p->device >= 0) {
+        int cur = -1;
+        if (cudaGetDevice(&cur) != cudaSuccess || cur != p->device) {
+            cudaGetLastError();
+            set_error("current device %d != the plan's device %d", cur, p->device);
+            return VX_ERR_INVALID;
+        }
+    }
+    vx_choice ch;
+    int64_t tiles = 0;
+    vx_status s = select_varlen(p, cu_host, ngroups, force_rung, &ch, &tiles);
+    if (s != VX_OK) return s;
+    if (used) *used = ch;
+    if (tiles == 0) return VX_OK;
+    VarSpec v{cu_dev, ngroups, tiles};
+    return launch(p, ch, 1, total, total, K, Q, total * K, Kt, total * K, S, total * total, stream,
+                  nullptr, &v);
 }
 
 vx_status vx_gemm_host(vx_plan_t p, int64_t batch, int64_t M, int64_t N, int64_t K,

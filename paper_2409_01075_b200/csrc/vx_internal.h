@@ -123,6 +123,12 @@ struct GatherSpec {
     void* dst[8];
     int64_t row0;
 };
+// ragged (varlen) attention batch (vx_gemm_varlen)
+struct VarSpec {
+    const int* cu_dev;   // device copy of the sequence offsets (ngroups + 1)
+    int32_t ngroups;
+    int64_t tiles;       // total tiles over every sequence
+};
 // candidate filters of the runtime selection
 enum SelectFilter : int32_t {
     kSelectAll = 0,
@@ -138,6 +144,10 @@ void set_error(const char* fmt, ...);
 // vx_dispatch.cu
 vx_status launch(const vx_plan_s* p, const vx_choice& ch, int64_t batch, int64_t M, int64_t N,
                  int64_t K, const void* A, int64_t sA, const void* B, int64_t sB, void* C,
-                 int64_t sC, void* stream, const GatherSpec* gather = nullptr);
+                 int64_t sC, void* stream, const GatherSpec* gather = nullptr,
+                 const VarSpec* var = nullptr);
+// vx_plan.cpp: runtime selection for a ragged batch of sequence lengths (host offsets cu)
+vx_status select_varlen(const vx_plan_s* p, const int32_t* cu, int32_t ngroups,
+                        int32_t force_rung, vx_choice* out, int64_t* tiles);
 vx_status prepare_kernels(const vx_plan_s* p);
 }  // namespace vx

@@ -377,6 +377,75 @@ static void rung_cost(const vx_plan_s* p, const Rung& r, int s, int64_t batch, i
     o->cost = cost;
 }
 
+// Ragged batch (the varlen reading of BASELINE config 4): S_g = Q_g K_g^T
+// for sequences of lengths s_g.  Eqs. 2-4 with the grid's aggregates: W = sum_g tiles_g
+// (tiles cover each sequence separately: padding only at each sequence's edge), unique
+// operand bytes in_b * K * 2 sum_g s_g, output bytes out_b * sum_g s_g^2; the persistent
+// schedule's grid-level Eq. 2 (R11) and the stagger (R21) as for the uniform rungs.
+static void varlen_cost(const vx_plan_s* p, const Rung& r, const int32_t* cu, int32_t ng,
+                        vx_choice* o, int64_t* padded) {
+    const vx_device_desc& d = p->desc;
+    const Calib& cal = p->cal.glob;
+    const int in_b = in_bytes(p->in), out_b = out_bytes(p->out);
+    const int64_t bm = r.bm, bn = r.bn, bk = r.bk, K = p->K;
+    int64_t tiles = 0, rows = 0, outs = 0, pad = 0;
+    for (int32_t g = 0; g < ng; ++g) {
+        const int64_t s = (int64_t)cu[g + 1] - cu[g];
+        const int64_t tg = cdiv(s, bm) * cdiv(s, bn);
+        tiles += tg;
+        rows += s;
+        outs += s * s;
+        pad += cdiv(s, bm) * bm * cdiv(s, bn) * bn;
+    }
+    const int64_t kb = cdiv(K, bk);
+    const int64_t slots = (int64_t)d.max_active_clusters[0];
+    const int64_t W = std::max<int64_t>(tiles, 1);
+    const int64_t F = eq3(W, slots);
+    const int64_t inner = t_move(bm * bn * bk, r.mac_milli);
+    const int64_t l_smem = t_move((bm + bn) * bk * in_b, r.l2s_milli);
+    const int64_t l_hbm = t_move((int64_t)in_b * K * 2 * rows, F * kb * cal.hbm_milli);
+    const int64_t tl = std::max(l_smem, l_hbm);
+    const int64_t ts = std::max(t_move(bm * bn * out_b, r.epi_milli),
+                                t_move((int64_t)out_b * outs, F * cal.hbm_milli));
+    const int64_t T = eq2(tl, kb, inner, ts);
+    int64_t cost = eq2(T - ts, F, ts, 0) + r.fixed;
+    if (std::min(W, slots) > d.sm_count / 2) cost += cal.stagger;
+    o->rung_id = r.rung_id; o->split = 1; o->family = r.family; o->swap = 0;
+    o->bm = r.bm; o->bn = r.bn; o->stages = r.stages;
+    o->tiles_m = 0; o->tiles_n = 0; o->grid = (int32_t)std::min(W, slots);
+    o->cluster = 1; o->mc = 1;
+    o->cost = cost;
+    *padded = pad;
+}
+
+vx_status select_varlen(const vx_plan_s* p, const int32_t* cu, int32_t ng, int32_t force_rung,
+                        vx_choice* out, int64_t* tiles) {
+    bool have = false;
+    vx_choice best{};
+    int64_t best_pad = 0;
+    for (const Rung& r : p->rungs) {
+        // candidates: non-swapped cta_group::1 tcgen05 tiles, persistent (the varlen
+        // epilogue stores each sequence's block from registers)
+        if (r.family != kUmma || r.cg != 1 || r.mc != 1 || r.occ != 1) continue;
+        if (force_rung >= 0 && r.rung_id != force_rung) continue;
+        vx_choice c;
+        int64_t pad = 0;
+        varlen_cost(p, r, cu, ng, &c, &pad);
+        if (!have || std::make_tuple(c.cost, pad, c.rung_id) < std::make_tuple(best.cost, best_pad, best.rung_id)) {
+            best = c; best_pad = pad; have = true;
+        }
+    }
+    if (!have) { set_error("rung %d cannot run a ragged batch", force_rung); return VX_ERR_INVALID; }
+    int64_t t = 0;
+    for (int32_t g = 0; g < ng; ++g) {
+        const int64_t s = (int64_t)cu[g + 1] - cu[g];
+        t += cdiv(s, best.bm) * cdiv(s, best.bn);
+    }
+    *tiles = t;
+    *out = best;
+    return VX_OK;
+}
+
 static inline int64_t padded_work(const vx_choice& c, int64_t batch) {
     // a multicast cluster pads its tile count to a multiple of mc along the non-shared axis
     const int64_t tm = (c.mc > 1 && c.swap) ? cdiv(c.tiles_m, c.mc) * c.mc : c.tiles_m;
@@ -616,6 +685,15 @@ vx_status vx_plan_destroy(vx_plan_t plan) {
 
 vx_status vx_plan_select(vx_plan_t plan, int64_t batch, int64_t M, int64_t N, vx_choice* out) {
     return select_choice(plan, batch, M, N, -1, 0, out);
+}
+
+vx_status vx_plan_select_varlen(vx_plan_t plan, int32_t ngroups, const int32_t* cu,
+                                vx_choice* out) {
+    if (!plan || !cu || !out || ngroups < 1) { set_error("NULL argument or ngroups < 1"); return VX_ERR_INVALID; }
+    for (int32_t g = 0; g < ngroups; ++g)
+        if (cu[g + 1] < cu[g]) { set_error("cu_seqlens must be non-decreasing"); return VX_ERR_INVALID; }
+    int64_t tiles = 0;
+    return select_varlen(plan, cu, ngroups, -1, out, &tiles);
 }
 
 vx_status vx_plan_cost(vx_plan_t plan, int32_t rung_id, int32_t split, int64_t batch,

@@ -72,6 +72,11 @@ struct UmmaParams {
     int a_bytes;                // bytes of A one stage loads: the whole A tile, or for M < 16
                                 // a short box of round_up(M, 8) rows (DESIGN.md 4.1 "short
                                 // A boxes"); the tile rows past it are never stored
+    const int* cu;              // ragged batch: > 0 groups = varlen mode --
+    int ngroups;                // sequence g has rows [cu[g], cu[g+1]) of the packed A (Q)
+                                // and B (K^T, N x K); S_g = Q_g K_g^T is s_g x s_g row-major
+                                // at element sum_{j<g} s_j^2 of C; tiles enumerate every
+                                // sequence's (tp, tq) in order (non-swapped, persistent)
     int ndst;                   // fused GEMM + row all-gather: > 0 = the
                                 // epilogue writes every finished C row chunk straight from
                                 // registers into rows dst_row0 + m of each dst[d] (peer /
@@ -214,6 +219,39 @@ __device__ __forceinline__ void decode_ctile(int tile, int tiles_p, int tiles_q,
         decode_tile(tile, (tiles_p + MC - 1) / MC, tiles_q, b, tp, tq);
         tp = tp * MC + (int)crank;
     }
+}
+
+// varlen mode: tile -> (tp, tq) within its sequence, the sequence's length, first packed row
+// and offset of its S block; O(groups) per call, groups are few (attention batch)
+struct VarTile {
+    int len, row0;
+    long long coff;
+};
+template <int BN>
+__device__ __forceinline__ void decode_varlen(int tile, const int* cu, int ng, int& tp, int& tq,
+                                              VarTile& v) {
+    long long coff = 0;
+    int t = tile;
+    int prev = __ldg(cu);
+    for (int g = 0; g < ng; ++g) {
+        const int next = __ldg(cu + g + 1);
+        const int len = next - prev;
+        const int tn = (len + BN - 1) / BN;
+        const int nt = ((len + 127) / 128) * tn;
+        if (t < nt) {
+            tp = t / tn;
+            tq = t - tp * tn;
+            v.len = len;
+            v.row0 = prev;
+            v.coff = coff;
+            return;
+        }
+        t -= nt;
+        coff += (long long)len * len;
+        prev = next;
+    }
+    tp = tq = 0;
+    v.len = 0; v.row0 = 0; v.coff = 0;
 }
 
 __device__ __forceinline__ uint32_t pack2(float a, float b, int kind) {
@@ -485,14 +523,16 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
             auto dep_wait = [&](int tile_, int kb_, int nleft) {
                 if (waited) return;
                 if (pid == 0 && !(p.dbg & 128) && !p.bpack && !P_MN && !Q_MN) {
-                    int b_, tp_, tq_;
-                    decode_ctile<SWAP, MC>(tile_, p.tiles_p, p.tiles_q, crank, b_, tp_, tq_);
+                    int b_ = 0, tp_, tq_;
+                    VarTile v_{0, 0, 0};
+                    if (p.ngroups) decode_varlen<BN>(tile_, p.cu, p.ngroups, tp_, tq_, v_);
+                    else decode_ctile<SWAP, MC>(tile_, p.tiles_p, p.tiles_q, crank, b_, tp_, tq_);
                     // this CTA's own rows (its half of a pair, its 1/MC share of the
                     // multicast operand): the maps' boxes are sized to them
                     const int pp = PAIR ? tp_ * 256 + (int)prank * 128
-                                 : tp_ * 128 + (MCP ? (int)crank * (128 / MC) : 0);
+                                 : tp_ * 128 + v_.row0 + (MCP ? (int)crank * (128 / MC) : 0);
                     const int qq = PAIR ? tq_ * BN + (int)prank * (BN / 2)
-                                 : tq_ * BN + (MCQ ? (int)crank * (BN / MC) : 0);
+                                 : tq_ * BN + v_.row0 + (MCQ ? (int)crank * (BN / MC) : 0);
                     const int n = nleft < S ? nleft : S;
                     for (int kb2 = kb_; kb2 < kb_ + n; ++kb2) {
                         ptx::tma_prefetch_3d(&tmP, kb2 * 64, pp, b_);
@@ -507,8 +547,10 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
             if (pid == 0) cyc_at(p, 21, cy0);
             int tile, k0, nk;
             while (wi.next(p, tile, k0, nk)) {
-                int b, tp, tq;
-                decode_ctile<SWAP, MC>(tile, p.tiles_p, p.tiles_q, crank, b, tp, tq);
+                int b = 0, tp, tq;
+                VarTile vt{0, 0, 0};   // varlen: the sequence's first packed row offsets P and Q
+                if (p.ngroups) decode_varlen<BN>(tile, p.cu, p.ngroups, tp, tq, vt);
+                else decode_ctile<SWAP, MC>(tile, p.tiles_p, p.tiles_q, crank, b, tp, tq);
                 if (pid == 0 && j == 0) cyc_at(p, 22, cy0);
                 for (int kb = k0; kb < k0 + nk; ++kb, ++j) {
                     // a unit is one k-block, or two (deep-K) when the next k-block of this
@@ -578,8 +620,8 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
                         ptx::mbar_arrive(&full[stage + 1]);
                         dep_wait(tile, kb, k0 + nk - kb);
                         if (!stamped && kb == k0) trace_at(p, 11);
-                        ptx::tma_load_4d(dP, &tmP2, &full[stage], 0, tp * 128, kb, b, pol);
-                        ptx::tma_load_4d(dQ, &tmQ2, &full[stage], 0, tq * BN, kb, b, pol);
+                        ptx::tma_load_4d(dP, &tmP2, &full[stage], 0, tp * 128 + vt.row0, kb, b, pol);
+                        ptx::tma_load_4d(dQ, &tmQ2, &full[stage], 0, tq * BN + vt.row0, kb, b, pol);
                         ++kb;
                         stage += 2;
                         if (stage == S) { stage = 0; phase ^= 1; }
@@ -617,7 +659,7 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
                         ptx::tma_load_3d_mc(dP + crank * (kP / MC), &tmP, &full[stage], kb * 64,
                                             tp * 128 + (int)crank * (128 / MC), b, kMcMask, pol);
                     } else {
-                        ptx::tma_load_3d(dP, &tmP, &full[stage], kb * 64, tp * 128, b, pol);
+                        ptx::tma_load_3d(dP, &tmP, &full[stage], kb * 64, tp * 128 + vt.row0, b, pol);
                     }
                     if (Q_MN) {
 #pragma unroll
@@ -629,7 +671,7 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
                         ptx::tma_load_3d_mc(dQ + crank * (kQ / MC), &tmQ, &full[stage], kb * 64,
                                             tq * BN + (int)crank * (BN / MC), b, kMcMask, pol);
                     } else {
-                        ptx::tma_load_3d(dQ, &tmQ, &full[stage], kb * 64, tq * BN, b, pol);
+                        ptx::tma_load_3d(dQ, &tmQ, &full[stage], kb * 64, tq * BN + vt.row0, b, pol);
                     }
                     if (++stage == S) { stage = 0; phase ^= 1; }
                 }
@@ -751,8 +793,10 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
         int tile, k0, nk;
         const long long U = (long long)p.num_tiles * p.kb_total;
         for (; wi.next(p, tile, k0, nk); ++it) {
-            int b, tp, tq;
-            decode_ctile<SWAP, MC>(tile, p.tiles_p, p.tiles_q, crank, b, tp, tq);
+            int b = 0, tp, tq;
+            VarTile vt{0, 0, 0};
+            if (p.ngroups) decode_varlen<BN>(tile, p.cu, p.ngroups, tp, tq, vt);
+            else decode_ctile<SWAP, MC>(tile, p.tiles_p, p.tiles_q, crank, b, tp, tq);
             // first P-axis row of this CTA's accumulator rows (a pair splits 256 rows)
             const int prow0 = PAIR ? tp * 256 + (int)prank * 128 : tp * 128;
             // ---- stream-K bookkeeping (before the accumulator wait) ---------------------
@@ -827,7 +871,7 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
                 }
                 continue;
             }
-            if (p.vec && p.ndst == 0 && !(p.dbg & 8)) {
+            if (p.vec && p.ndst == 0 && p.ngroups == 0 && !(p.dbg & 8)) {
                 // TMEM -> registers -> swizzled SMEM staging -> TMA bulk store (full lines,
                 // asynchronous, M/N tails clipped by the tensor map)
                 const int ob = p.out_kind == 2 ? 4 : 2;
@@ -919,8 +963,16 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
                 continue;
             }
             const int pr = prow0 + row;  // global index on the P axis
-            char* Cb = reinterpret_cast<char*>(p.C) +
-                       (long long)b * p.sC * (p.out_kind == 2 ? 4 : 2);
+            const int ob_ = p.out_kind == 2 ? 4 : 2;
+            // varlen: this sequence's s x s block of C (vector stores iff its rows are 16-B
+            // aligned); otherwise the batch's M x N matrix
+            char* Cb = reinterpret_cast<char*>(p.C) + (p.ngroups ? vt.coff * ob_ : (long long)b * p.sC * ob_);
+            const int Me = p.ngroups ? vt.len : p.M;
+            const int Ne = p.ngroups ? vt.len : p.N;
+            const long long ldc_e = p.ngroups ? vt.len : p.ldc;
+            const bool vec_e = p.ngroups ? ((vt.len * ob_) % 16 == 0 && (vt.coff * ob_) % 16 == 0 &&
+                                            (reinterpret_cast<uintptr_t>(p.C) & 15) == 0)
+                                         : p.vec != 0;
 #pragma unroll 1
             for (int c = grp; c < (BN + 31) / 32; c += NG) {
                 uint32_t v[32];
@@ -934,7 +986,7 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
                     if (f[0] == 12345.f) store1(Cb, 0, f[1], p.out_kind);
                 } else if (!SWAP) {
                     // row pr = m, columns = n
-                    if (pr < p.M) {
+                    if (pr < Me) {
                         const int n0 = tq * BN + c * 32;
                         if (p.ndst > 0) {
                             // fused all-gather: the same chunk into every destination, at
@@ -948,9 +1000,9 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
                                 else store_row_scalar(Db, base, n0, p.N, W, f, p.out_kind);
                             }
                         } else {
-                            const long long base = (long long)pr * p.ldc;
-                            if (p.vec) store_row_chunk<W>(Cb, base, n0, p.N, f, p.out_kind);
-                            else store_row_scalar(Cb, base, n0, p.N, W, f, p.out_kind);
+                            const long long base = (long long)pr * ldc_e;
+                            if (vec_e) store_row_chunk<W>(Cb, base, n0, Ne, f, p.out_kind);
+                            else store_row_scalar(Cb, base, n0, Ne, W, f, p.out_kind);
                         }
                     }
                 } else if (pr < p.N) {

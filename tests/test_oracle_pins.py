@@ -115,3 +115,13 @@ def test_gemv_rungs_only_hold_m_up_to_mt():
     table = {"in": "bf16", "out": "bf16", "rungs": [g, t]}
     assert S.select(table, 1, 4, 1000, 3072, CV["desc"], cal)["rung_id"] == 0
     assert S.select(table, 1, 5, 1000, 3072, CV["desc"], cal)["rung_id"] == 1
+
+
+@pytest.mark.parametrize("case", CV["varlen_cost"], ids=[c["name"] for c in CV["varlen_cost"]])
+def test_varlen_cost_worked_examples(case):
+    """Ragged attention batch: Eqs. 2-4 over the ragged tile set
+    (DESIGN.md 5.1 V1)."""
+    cal = dict(CV["calib"], **case.get("calib_override", {}))
+    c = S.varlen_cost(_rung(case["rung"]), case["lens"], case["K"], "bf16", "bf16", CV["desc"], cal)
+    for k, v in case["want"].items():
+        assert c[k] == v, (case["name"], k, c[k], v)

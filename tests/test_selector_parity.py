@@ -155,3 +155,23 @@ def test_calibration_missing_key_rejected():
     with pytest.raises(vx.VxError) as e:
         vx.Plan(3072, 768, "bf16", "bf16", "nk", desc=DESC, calib=c)
     assert e.value.status == 2
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_varlen_selection_matches_oracle(d):
+    """vx_plan_select_varlen (ragged attention batch) is bit-identical to
+    the oracle's select_varlen on random length mixes, single sequences and empty ones."""
+    import random
+    p = vx.Plan(0, d, "bf16", "bf16", "nk", desc=DESC)
+    t = _oracle_table(d, "bf16", "bf16")
+    rnd = random.Random(d)
+    mixes = [[1], [2048], [0, 5, 0], [128, 128, 128]]
+    mixes += [[rnd.randint(1, 2048) for _ in range(rnd.randint(1, 32))] for _ in range(40)]
+    for lens in mixes:
+        cu = [0]
+        for s in lens:
+            cu.append(cu[-1] + s)
+        got = p.select_varlen(cu)
+        want = S.select_varlen(t, lens, d, DESC_J, CAL)
+        assert (got["rung_id"], got["cost"], got["grid"]) == (want["rung_id"], want["cost"],
+                                                              want["grid"]), lens

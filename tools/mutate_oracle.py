@@ -81,6 +81,14 @@ MUTATIONS = [
     ("_streamk_cost", "pairs share units per CTA instead of per pair",
      "# units go to CTAs, or to CTA pairs\n    G = min(desc[\"max_active_clusters\"][str(cg)], U)",
      "# units go to CTAs, or to CTA pairs\n    G = min(desc[\"max_active_clusters\"][\"1\"], U)"),
+    ("varlen_cost", "ragged tiles from the total length (padding across sequences)",
+     "    tiles = sum(ceil_div(s, bm) * ceil_div(s, bn) for s in lens)",
+     "    tiles = ceil_div(sum(lens), bm) * ceil_div(max(lens), bn)"),
+    ("varlen_cost", "ragged output bytes from the packed total squared",
+     "    outs = sum(s * s for s in lens)", "    outs = sum(lens) ** 2"),
+    ("varlen_cost", "ragged operands counted once instead of Q and K",
+     "    l_hbm = t_load(in_b * K * 2 * rows, F * kb * hbm)",
+     "    l_hbm = t_load(in_b * K * rows, F * kb * hbm)"),
     ("_gemv_cost", "GEMV residency 2 CTAs / SM instead of 4",
      "    F = parallel_factor(tiles, desc[\"sm_count\"] * GEMV_OCC)",
      "    F = parallel_factor(tiles, desc[\"sm_count\"] * 2)"),
