@@ -140,8 +140,28 @@ class ClockSampler:
 # ----------------------------------------------------------------------------------------
 # distributed plumbing
 # ----------------------------------------------------------------------------------------
+def self_launch(args):
+    """--gpus N > 1 without torchrun: re-launch this script under torch.distributed.run with
+    N ranks on this node (127.0.0.1 rendezvous) and forward its exit code; never silently
+    fall back to one GPU."""
+    import socket
+    n = torch.cuda.device_count()
+    if n < args.gpus:
+        print(json.dumps({"metric": METRIC, "error": "--gpus %d but only %d visible GPUs"
+                          % (args.gpus, n)}), flush=True)
+        sys.exit(2)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           "--nproc-per-node", str(args.gpus), "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
 def dist_init(n_gpus):
-    if n_gpus <= 1 or "RANK" not in os.environ:
+    if n_gpus <= 1:
         return 0, 1, 0
     import torch.distributed as dist
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
@@ -171,6 +191,16 @@ def allreduce_max(vals, world):
 # the oracle arm (cpu_baseline and --impl reference)
 # ----------------------------------------------------------------------------------------
 _ORACLE_B = {}
+
+
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def oracle_sample(budget_flops: float, threads: int = 0):
@@ -426,6 +456,11 @@ def run_mine(args, rank, world, local):
     roof["peak_source"] = peaks["source"] + (" sustained" if tensor_bound else "")
 
     sharded = run_sharded(args, rank, world, local, vx, stream, side, l2)
+    extra = None
+    if not args.no_extra:
+        extra = {"attention": run_attention(vx, stream, side, rank, world),
+                 "fp32_config1": run_fp32(vx, stream),
+                 "isolated": run_isolated(vx, plans, pts, stream, rows)}
     e2e = None if args.no_e2e else run_e2e(args, rank, world, local, vx, plans, pts, stream)
     cublas = None
     if world == 1 and not args.no_cublas:
@@ -447,10 +482,14 @@ def run_mine(args, rank, world, local):
         if world == 1 and not args.no_cpu:
             s_, nthr = oracle_sample(args.ref_budget)
             r = [f / t / 1e12 for f, t in s_]
+            s1, _ = oracle_sample(args.ref_budget / 16, threads=1)
+            r1 = [f / t / 1e12 for f, t in s1]
             cpu = {"value": geomean(r), "unit": UNIT, "cores": nthr, "kind": "oracle",
+                   "cpu_model": cpu_model(), "one_thread_value": geomean(r1),
                    "sample": "fp64 oracle (oracle/gemm_ref.c): for each of the 6 (N,K) of the "
                              "sweep, its smallest and largest M, a row subset (>= %d rows, "
-                             "~%.1e flops total); geomean of per-sample TFLOP/s" % (
+                             "~%.1e flops total); geomean of per-sample TFLOP/s; "
+                             "one_thread_value: same on 1 thread, 1/16 of the flops" % (
                                  nthr, args.ref_budget)}
         result = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -476,6 +515,7 @@ def run_mine(args, rank, world, local):
                      "roof_frac_geomean_all": geomean([r["roof_frac"] for r in rows]),
                      "peaks": peaks},
             "sharded": sharded,
+            "configs_extra": extra,
             "e2e": e2e,
             "cpu_baseline": cpu,
             "cublas_ref": cublas,
@@ -488,6 +528,166 @@ def run_mine(args, rank, world, local):
                 json.dump(rows, f, indent=1)
         print(json.dumps(result), flush=True)
     return result
+
+
+def run_attention(vx, stream, side, rank, world):
+    """configs[3]: batched attention scores S_b = Q_b K_b^T, batch 32, s swept, d in {64,128}
+    (bf16 in / bf16 out; always HBM-bound: the S write dominates), timed like the sweep
+    (one graph, R launches per point over fresh arena slices); plus the ragged (varlen)
+    reading -- 32 sequences of mixed lengths in ONE vx_gemm_varlen launch per step."""
+    pts_a = [(s, d) for d in synth.ATTN_D for s in synth.ATTN_S]
+    peaks = load_peaks()
+    res = {"points": [], "how": "graph of %d launches per point on fresh slices, cold L2" % 8}
+    B = synth.ATTN_BATCH
+    for d in synth.ATTN_D:
+        p = vx.Plan(0, d, "bf16", "bf16", "nk", device=stream.device.index)
+        items = [(p, s, s, d) for s in synth.ATTN_S]
+        GiB = 1 << 29
+        aA = Arena(max(GiB, 4 * B * max(synth.ATTN_S) * d), stream.device, "normal", 300 + rank)
+        aB = Arena(max(GiB, 4 * B * max(synth.ATTN_S) * d), stream.device, "normal", 400 + rank,
+                   scale=d ** -0.5)
+        aC = Arena(max(GiB, 2 * B * max(synth.ATTN_S) ** 2), stream.device, "empty", 0)
+        g = BatchedGraph(items, 8, (aA, aB, aC), stream, side, B)
+        for _ in range(3):
+            g.replay()
+        torch.cuda.synchronize()
+        samples = []
+        for _ in range(5):
+            g.replay()
+            torch.cuda.synchronize()
+            samples.append(g.per_launch_ms())
+        per = [statistics.median(s_[j] for s_ in samples) for j in range(len(items))]
+        per = allreduce_max(per, world)
+        for (pl, s, _, _), ms in zip(items, per):
+            fl = flops(s, s, d, B)
+            by = algo_bytes(s, s, d, B)
+            res["points"].append({"d": d, "s": s, "us": ms * 1e3, "tflops": fl / (ms * 1e-3) / 1e12,
+                                  "gbs": by / (ms * 1e-3) / 1e9,
+                                  "hbm_frac": by / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"]})
+        del g, aA, aB, aC
+    big = [x for x in res["points"] if x["s"] >= 512]
+    res["hbm_frac_geomean_s>=512"] = geomean([x["hbm_frac"] for x in big])
+    res["tflops_geomean"] = geomean([x["tflops"] for x in res["points"]])
+    # ragged batch: 32 sequences with lengths drawn (seeded) from 1..2048, one launch
+    import random
+    rnd = random.Random(2409)
+    lens = [rnd.randint(1, 2048) for _ in range(B)]
+    cu = [0]
+    for s in lens:
+        cu.append(cu[-1] + s)
+    rg = {}
+    for d in synth.ATTN_D:
+        p = vx.Plan(0, d, "bf16", "bf16", "nk", device=stream.device.index)
+        Q = synth.matrix((cu[-1], d), "bf16", "normal", seed=5, device=stream.device)
+        Kt = synth.matrix((cu[-1], d), "bf16", "normal", seed=6, scale=d ** -0.5, device=stream.device)
+        S = torch.empty(sum(s * s for s in lens), dtype=torch.bfloat16, device=stream.device)
+        for _ in range(3):
+            p.gemm_varlen(Q, Kt, cu, out=S)
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(10):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            p.gemm_varlen(Q, Kt, cu, out=S)
+            e1.record(stream)
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        ms = statistics.median(ts)
+        fl = sum(2.0 * s * s * d for s in lens)
+        by = sum(2 * (2 * s * d + s * s) for s in lens)
+        rg["d%d" % d] = {"us": ms * 1e3, "tflops": fl / (ms * 1e-3) / 1e12,
+                         "hbm_frac": by / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                         "choice": p.select_varlen(cu)}
+    res["ragged"] = {"lens_seed": 2409, "sequences": B, "tokens": cu[-1], "per_d": rg,
+                     "how": "one vx_gemm_varlen launch per step, CUDA events, median of 10"}
+    return res
+
+
+class BatchedGraph(SweepGraph):
+    """SweepGraph for batched items: R launches of vx_gemm_batched per point."""
+
+    def __init__(self, items, R, arenas, stream, side, batch):
+        import paper_2409_01075_b200 as vx
+        self.R = R
+        aA, aB, aC = arenas
+        work = [(plan, M, N, K, [(aA.take(batch * M * K), aB.take(batch * N * K),
+                                  aC.take(batch * M * N)) for _ in range(R)])
+                for plan, M, N, K in items]
+        side.wait_stream(stream)
+        with torch.cuda.stream(side):
+            sp = ctypes.c_void_p(side.cuda_stream)
+            for plan, M, N, K, ptrs in work:
+                a, b, c = ptrs[0]
+                plan.gemm_ptr(batch, M, N, K, a, M * K, b, N * K, c, M * N, sp)
+            side.synchronize()
+            self.events = [torch.cuda.Event(enable_timing=True, external=True)
+                           for _ in range(len(work) + 1)]
+            self.g = torch.cuda.CUDAGraph()
+            n0 = vx.launch_count()
+            with torch.cuda.graph(self.g, stream=side):
+                cs = torch.cuda.current_stream()
+                sp = ctypes.c_void_p(cs.cuda_stream)
+                for i, (plan, M, N, K, ptrs) in enumerate(work):
+                    self.events[i].record(cs)
+                    for a, b, c in ptrs:
+                        plan.gemm_ptr(batch, M, N, K, a, M * K, b, N * K, c, M * N, sp)
+                self.events[-1].record(cs)
+            self.launches = vx.launch_count() - n0
+        stream.wait_stream(side)
+
+
+def run_fp32(vx, stream):
+    """configs[0]: the fp32 CUDA-core path, M=37 (non-tile-multiple), N=K=64 (latency bound)."""
+    M, N, K = 37, 64, 64
+    p = vx.Plan(N, K, "fp32", "fp32", "kn", device=stream.device.index)
+    A, B = synth.gemm_inputs(M, N, K, "fp32", "kn", seed=1, device=stream.device)
+    C = torch.empty((M, N), dtype=torch.float32, device=stream.device)
+    for _ in range(10):
+        p.gemm(A, B, out=C)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(50):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        p.gemm(A, B, out=C)
+        e1.record(stream)
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ms = statistics.median(ts)
+    return {"M": M, "N": N, "K": K, "us": ms * 1e3, "gflops": flops(M, N, K) / (ms * 1e-3) / 1e9,
+            "choice": p.select(M), "how": "single launches, CUDA events, median of 50"}
+
+
+def run_isolated(vx, plans, pts, stream, rows):
+    """Per sweep point, ONE launch in isolation (L2 flushed by a 512 MB write before it,
+    nothing overlapping): the single-launch latency SURVEY 8(d) d4 asks for, next to the
+    back-to-back per-launch time of the sweep graph."""
+    flush = torch.empty(1 << 29, dtype=torch.uint8, device=stream.device)
+    GiB = 1 << 30
+    A = torch.empty(GiB // 4, dtype=torch.bfloat16, device=stream.device).normal_()
+    B = torch.empty(GiB // 4, dtype=torch.bfloat16, device=stream.device).normal_()
+    C = torch.empty(GiB // 4, dtype=torch.bfloat16, device=stream.device)
+    sp = ctypes.c_void_p(stream.cuda_stream)
+    out = []
+    for (tag, M, N, K), row in zip(pts, rows):
+        ts = []
+        for rep in range(4):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            plans[(N, K)].gemm_ptr(1, M, N, K, A.data_ptr(), M * K, B.data_ptr(), N * K,
+                                   C.data_ptr(), M * N, sp)
+            e1.record(stream)
+            e1.synchronize()
+            if rep:
+                ts.append(e0.elapsed_time(e1))
+        row["us_isolated"] = statistics.median(ts) * 1e3
+        out.append(row["us_isolated"])
+    del flush, A, B, C
+    return {"us_isolated_geomean": geomean(out),
+            "us_back_to_back_geomean": geomean([r["us"] for r in rows]),
+            "how": "one launch after a 512 MB L2 flush, CUDA events around it (includes the "
+                   "launch latency), median of 3; per point in --points-out as us_isolated"}
 
 
 def run_cublas_ref(pts, stream, side, rank, R, steps):
@@ -558,9 +758,9 @@ def selector_overhead(vx, plans_nk, local):
 
 def run_sharded(args, rank, world, local, vx, stream, side, l2):
     """configs[4]: M=65536, N=11008, K=4096 rows split over the ranks (no collective)."""
+    from paper_2409_01075_b200.dist import row_shard
     M, N, K = 65536, 11008, 4096
-    lo = rank * M // world
-    hi = (rank + 1) * M // world
+    lo, hi = row_shard(M, world, rank)
     m = hi - lo
     p = vx.Plan(N, K, "bf16", "bf16", "nk", device=local)
     R = R_PER_POINT
@@ -579,8 +779,27 @@ def run_sharded(args, rank, world, local, vx, stream, side, l2):
     del g, arenas
     out = {"M": M, "N": N, "K": K, "rows_per_rank": m, "ms": t,
            "tflops": flops(M, N, K) / (t * 1e-3) / 1e12, "rung": ch["rung_id"],
-           "split": ch["split"], "gather": False, "launches_per_sample": R}
+           "split": ch["split"], "gather": False, "launches_per_sample": R,
+           "scaling": "strong (identical M=65536 problem, rows split over the ranks)"}
     if world > 1:
+        # T_1: the whole problem on ONE GPU of the same box (rank 0; the others wait), so
+        # the strong-scaling ratio T_1 / T_P is measured in the same run
+        t1 = 0.0
+        if rank == 0:
+            arenas1 = make_arenas([("", M, N, K)], stream.device, rank)
+            g1 = SweepGraph([(p, M, N, K)], 4, arenas1, stream, side)
+            g1.replay()
+            torch.cuda.synchronize()
+            t1s = []
+            for _ in range(3):
+                g1.replay()
+                torch.cuda.synchronize()
+                t1s.append(g1.per_launch_ms()[0])
+            t1 = statistics.median(t1s)
+            del g1, arenas1
+        t1 = allreduce_max([t1], world)[0]
+        out["ms_1gpu_full"] = t1
+        out["strong_scaling_compute"] = t1 / t
         # optional gathered C: GEMM of this rank's rows, then ONE NCCL
         # all_gather_into_tensor of the row shards; timed separately (communication-bound)
         from paper_2409_01075_b200.dist import gather_rows
@@ -604,6 +823,30 @@ def run_sharded(args, rank, world, local, vx, stream, side, l2):
         out["gathered_ms"] = tg
         out["gathered_tflops"] = flops(M, N, K) / (tg * 1e-3) / 1e12
         out["gathered_bytes_per_rank"] = 2 * (M - m) * N
+        out["strong_scaling_gathered_nccl"] = out["ms_1gpu_full"] / tg
+        # fused GEMM + all-gather: the epilogue writes every finished C
+        # chunk into every rank's symmetric-memory C over NVLink; no separate collective
+        try:
+            from paper_2409_01075_b200.dist import fused_gather_gemm, symmetric_gather_buffer
+            buf = symmetric_gather_buffer(M, N, torch.bfloat16, stream.device)
+            fts = []
+            for i in range(4):
+                barrier(world)
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                fused_gather_gemm(p, A, B, M, buf=buf)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                if i:
+                    fts.append(e0.elapsed_time(e1))
+            tf = allreduce_max([statistics.median(fts)], world)[0]
+            out["fused_gathered_ms"] = tf
+            out["fused_gathered_tflops"] = flops(M, N, K) / (tf * 1e-3) / 1e12
+            out["strong_scaling_gathered_fused"] = out["ms_1gpu_full"] / tf
+            del buf
+        except Exception as e:   # symmetric memory needs NVLink P2P: report, do not fake
+            out["fused_gathered_error"] = repr(e)[:200]
         del A, B, C, full
     return out
 
@@ -680,7 +923,11 @@ def main():
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-staged e2e leg")
     ap.add_argument("--no-cublas", action="store_true",
                     help="skip the informational cuBLAS line (torch.mm on the same points)")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="skip the attention / fp32 / isolated-launch lines")
     args = ap.parse_args()
+    if args.gpus > 1 and "RANK" not in os.environ:
+        self_launch(args)
     if args.warmup < 3 and args.impl == "mine":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
     if args.impl == "reference":

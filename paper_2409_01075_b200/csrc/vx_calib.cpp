@@ -23,34 +23,34 @@ namespace vx {
 
 static const Calib kCalib = {
     /*hbm_milli=*/3327023,   // 6543 GB/s measured copy bandwidth / 1.965 GHz
-    /*dsm_milli=*/2931,      // effective in-cluster reduce rate (fitted)
-    /*fixed_cluster=*/2538,  // cluster launch + two cluster barriers (fitted)
+    /*dsm_milli=*/3539,      // effective in-cluster reduce rate (fitted)
+    /*fixed_cluster=*/652,  // cluster launch + two cluster barriers (fitted)
     /*skfix_milli=*/13315,   // stream-K partial write + read-back (fitted)
-    /*stagger=*/4000,       // first wave > sm_count / 2 CTAs, back to back (R21; fitted)
+    /*stagger=*/3478,       // first wave > sm_count / 2 CTAs, back to back (R21; fitted)
 };
 
 static const RungCalib kRungs[] = {
-    {"umma_128x64", 1000367, 46603, 8000, 7014},
-    {"umma_128x128", 1520875, 160000, 8000, 371},
+    {"umma_128x64", 1000367, 46603, 8000, 6919},
+    {"umma_128x128", 1596919, 115222, 12267, 429},
     {"umma_128x256", 1923790, 160000, 30923, 200},
-    {"umma_256x128", 3611307, 86550, 25081, 3481},
-    {"umma_256x64", 2323400, 160000, 40405, 11183},
-    {"umma_256x256", 4096000, 146087, 70638, 1233},
-    {"umma_swap_128x16", 2468107, 33673, 9200, 4053},
-    {"umma_swap_128x32", 1000000, 45735, 15471, 4110},
-    {"umma_swap_128x64", 1183082, 56182, 11212, 2864},
-    {"umma_swap_128x128", 1837162, 51409, 14512, 1635},
+    {"umma_256x128", 3611307, 86550, 93781, 3027},
+    {"umma_256x64", 2423501, 160000, 56567, 9724},
+    {"umma_256x256", 4096000, 160000, 77365, 1174},
+    {"umma_swap_128x16", 1000000, 44897, 10901, 4053},
+    {"umma_swap_128x32", 1000000, 43557, 9152, 3404},
+    {"umma_swap_128x64", 1126745, 107013, 10678, 2864},
+    {"umma_swap_128x128", 1597532, 51409, 8000, 788},
     // BN = 192 / swapped BN = 192, 256 (tile-boundary cliffs, R6)
-    {"umma_128x192", 1470000, 106501, 34060, 200},
-    {"umma_swap_128x192", 1738143, 100193, 33920, 450},
-    {"umma_swap_128x256", 1936545, 160000, 29217, 450},
+    {"umma_128x192", 1400000, 160000, 49661, 200},
+    {"umma_swap_128x192", 1738143, 79876, 19110, 507},
+    {"umma_swap_128x256", 1936545, 160000, 27826, 338},
     // TMA-multicast clusters
-    {"umma_mc2_128x128", 1744850, 41151, 13097, 2547},
-    {"umma_mc2_128x256", 4096000, 38348, 512000, 3025},
-    {"umma_swap_mc2_128x32", 1000000, 36759, 8000, 3330},
-    {"umma_swap_mc2_128x64", 1050000, 40140, 512000, 7115},
-    {"umma_swap_mc4_128x64", 1000000, 36408, 512000, 6776},
-    {"gemv_1x8", 28714, 9151, 1000, 3332},
+    {"umma_mc2_128x128", 1884796, 41151, 39291, 2674},
+    {"umma_mc2_128x256", 4096000, 38348, 512000, 2762},
+    {"umma_swap_mc2_128x32", 1950476, 36460, 8000, 5361},
+    {"umma_swap_mc2_128x64", 1050000, 76964, 38169, 6454},
+    {"umma_swap_mc4_128x64", 2058000, 36408, 512000, 6776},
+    {"gemv_1x8", 23780, 9151, 1000, 3332},
     {"gemv_2x8", 8243, 43894, 1000, 3215},
     {"gemv_4x8", 8776, 64524, 1000, 2932},
     {"gemv_8x8", 10157, 5087, 148392, 497},
