@@ -459,7 +459,7 @@ def run_mine(args, rank, world, local):
     extra = None
     if not args.no_extra:
         extra = {"attention": run_attention(vx, stream, side, rank, world),
-                 "fp32_config1": run_fp32(vx, stream),
+                 "fp32_config1": run_fp32(vx, stream, side),
                  "isolated": run_isolated(vx, plans, pts, stream, rows)}
     e2e = None if args.no_e2e else run_e2e(args, rank, world, local, vx, plans, pts, stream)
     cublas = None
@@ -581,25 +581,16 @@ def run_attention(vx, stream, side, rank, world):
         Q = synth.matrix((cu[-1], d), "bf16", "normal", seed=5, device=stream.device)
         Kt = synth.matrix((cu[-1], d), "bf16", "normal", seed=6, scale=d ** -0.5, device=stream.device)
         S = torch.empty(sum(s * s for s in lens), dtype=torch.bfloat16, device=stream.device)
-        for _ in range(3):
-            p.gemm_varlen(Q, Kt, cu, out=S)
-        torch.cuda.synchronize()
-        ts = []
-        for _ in range(10):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            p.gemm_varlen(Q, Kt, cu, out=S)
-            e1.record(stream)
-            e1.synchronize()
-            ts.append(e0.elapsed_time(e1))
-        ms = statistics.median(ts)
+        cu_d = torch.tensor(cu, dtype=torch.int32, device=stream.device)
+        ms = graph_time(lambda: p.gemm_varlen(Q, Kt, cu, out=S, cu_dev=cu_d), stream, side, 8)
         fl = sum(2.0 * s * s * d for s in lens)
         by = sum(2 * (2 * s * d + s * s) for s in lens)
         rg["d%d" % d] = {"us": ms * 1e3, "tflops": fl / (ms * 1e-3) / 1e12,
                          "hbm_frac": by / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
                          "choice": p.select_varlen(cu)}
     res["ragged"] = {"lens_seed": 2409, "sequences": B, "tokens": cu[-1], "per_d": rg,
-                     "how": "one vx_gemm_varlen launch per step, CUDA events, median of 10"}
+                     "how": "graph of 8 back-to-back vx_gemm_varlen launches, CUDA events, "
+                            "median of 5 replays / 8"}
     return res
 
 
@@ -636,26 +627,42 @@ class BatchedGraph(SweepGraph):
         stream.wait_stream(side)
 
 
-def run_fp32(vx, stream):
+def graph_time(fn, stream, side, R, reps=5):
+    """Device time per call of `fn` (which launches on the current stream): R calls captured
+    in one CUDA graph, median over replays / R (host overhead excluded)."""
+    side.wait_stream(stream)
+    with torch.cuda.stream(side):
+        fn()
+        side.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=side):
+            for _ in range(R):
+                fn()
+    stream.wait_stream(side)
+    g.replay()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        g.replay()
+        e1.record(stream)
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1) / R)
+    del g
+    return statistics.median(ts)
+
+
+def run_fp32(vx, stream, side):
     """configs[0]: the fp32 CUDA-core path, M=37 (non-tile-multiple), N=K=64 (latency bound)."""
     M, N, K = 37, 64, 64
     p = vx.Plan(N, K, "fp32", "fp32", "kn", device=stream.device.index)
     A, B = synth.gemm_inputs(M, N, K, "fp32", "kn", seed=1, device=stream.device)
     C = torch.empty((M, N), dtype=torch.float32, device=stream.device)
-    for _ in range(10):
-        p.gemm(A, B, out=C)
-    torch.cuda.synchronize()
-    ts = []
-    for _ in range(50):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        p.gemm(A, B, out=C)
-        e1.record(stream)
-        e1.synchronize()
-        ts.append(e0.elapsed_time(e1))
-    ms = statistics.median(ts)
+    ms = graph_time(lambda: p.gemm(A, B, out=C), stream, side, 32)
     return {"M": M, "N": N, "K": K, "us": ms * 1e3, "gflops": flops(M, N, K) / (ms * 1e-3) / 1e9,
-            "choice": p.select(M), "how": "single launches, CUDA events, median of 50"}
+            "choice": p.select(M), "how": "graph of 32 back-to-back launches, median of 5 "
+                                          "replays / 32 (device time per launch)"}
 
 
 def run_isolated(vx, plans, pts, stream, rows):

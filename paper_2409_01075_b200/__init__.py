@@ -367,10 +367,11 @@ class Plan:
         return ch.as_dict() if want_choice else None
 
     def gemm_varlen(self, Q, Kt, cu_seqlens, out=None, stream=None, force: int = -1,
-                    want_choice: bool = False):
+                    want_choice: bool = False, cu_dev=None):
         """Ragged attention batch (vx_gemm_varlen): S_g = Q_g K_g^T for packed Q, Kt
-        [total, d] and cu_seqlens (list/tensor of ngroups + 1 offsets).  Returns the packed
-        S (sum_g s_g^2 elements)."""
+        [total, d] and cu_seqlens (host list of ngroups + 1 offsets; cu_dev: the same as a
+        device int32 tensor, made here if not given).  Returns the packed S (sum_g s_g^2
+        elements)."""
         import torch
         cu = [int(x) for x in (cu_seqlens.tolist() if hasattr(cu_seqlens, "tolist") else cu_seqlens)]
         ng = len(cu) - 1
@@ -386,8 +387,10 @@ class Plan:
         elif out.numel() < n_out or out.dtype != odt or not out.is_contiguous():
             raise ValueError("out must hold %d contiguous %s elements" % (n_out, odt))
         cu_h = (ctypes.c_int32 * len(cu))(*cu)
-        cu_d = torch.tensor(cu, dtype=torch.int32, device=Q.device)
-        self._cu_keep = cu_d          # keep alive until the launch has consumed it
+        if cu_dev is None:
+            cu_dev = torch.tensor(cu, dtype=torch.int32, device=Q.device)
+            self._cu_keep = cu_dev    # keep alive until the launch has consumed it
+        cu_d = cu_dev
         ch = Choice()
         _check(_lib.vx_gemm_varlen(self._h, ng, cu_h, cu_d.data_ptr(), self.K, Q.data_ptr(),
                                    Kt.data_ptr(), out.data_ptr(), force, _stream_ptr(stream),

@@ -24,6 +24,10 @@ static const int g_dbg = [] {                 // VX_DEBUG_FLAGS (kernel phase sk
     const char* e = getenv("VX_DEBUG_FLAGS");
     return e ? atoi(e) : 0;
 }();
+static const int g_group_p = [] {             // VX_GROUP_P: raster group size (experiments)
+    const char* e = getenv("VX_GROUP_P");
+    return e ? atoi(e) : 0;
+}();
 static const bool g_pdl = [] {                 // VX_PDL=0 disables programmatic launch
     const char* e = getenv("VX_PDL");
     return !(e && e[0] == '0');
@@ -476,6 +480,8 @@ vx_status launch(const vx_plan_s* p, const vx_choice& ch, int64_t batch, int64_t
     // (A/B timing only)
     // bytes of A landing in each CTA's stage: the short box, else the whole A tile (a
     // multicast cluster's sub-boxes from every CTA all land in every CTA's stage)
+    // raster group (P tiles swept over every Q tile while held in L2): VX_GROUP_P overrides
+    prm.group_p = g_group_p > 0 ? g_group_p : kGroupP;
     prm.a_bytes = (short_a ? a_box : (swap ? r.bn : 128)) * 64 * 2;
     prm.kdouble = (!b_mn && p->bl != VX_B_PACKED && K % 64 == 0 && K >= 128 && mc == 1 && !short_a &&
                    r.stages >= (pair ? 8 : 6) && !(g_dbg & 4096)) ? 1 : 0;

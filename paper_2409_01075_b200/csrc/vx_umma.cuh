@@ -83,6 +83,7 @@ struct UmmaParams {
                                 // symmetric-memory buffers over NVLink); C is not written
     long long dst_row0;
     void* dst[8];
+    int group_p;                // raster group: P tiles per group swept over all Q tiles (L2)
     int kdouble;                // 1: two-chunk loads (tmP2 / tmQ2) fill two adjacent ring
                                 // stages with one TMA box per operand (K % 64 == 0, K-major
                                 // P and Q, unpacked; rings of >= 6 stages, >= 8 for pair
@@ -181,7 +182,7 @@ __device__ __forceinline__ void cyc_at(const UmmaParams& p, int slot, long long 
     if (p.trace) p.trace[blockIdx.x * kTraceSlots + slot] = clock64() - base;
 }
 
-constexpr int kGroupP = 16;   // raster: 16 P-tiles x all Q-tiles per group (L2 reuse)
+constexpr int kGroupP = 16;   // default raster: 16 P-tiles x all Q-tiles per group (L2 reuse)
 
 template <int BN>
 struct UmmaCfg {
@@ -192,14 +193,14 @@ struct UmmaCfg {
 };
 
 __device__ __forceinline__ void decode_tile(int tile, int tiles_p, int tiles_q, int& b, int& tp,
-                                            int& tq) {
+                                            int& tq, int gp = kGroupP) {
     const int per_b = tiles_p * tiles_q;
     b = tile / per_b;
     const int t = tile - b * per_b;
-    const int group = t / (kGroupP * tiles_q);
-    const int first = group * kGroupP;
-    const int gsz = min(kGroupP, tiles_p - first);
-    const int local = t - group * kGroupP * tiles_q;
+    const int group = t / (gp * tiles_q);
+    const int first = group * gp;
+    const int gsz = min(gp, tiles_p - first);
+    const int local = t - group * gp * tiles_q;
     tp = first + local % gsz;
     tq = local / gsz;
 }
@@ -209,14 +210,14 @@ __device__ __forceinline__ void decode_tile(int tile, int tiles_p, int tiles_q, 
 // Q tile (swapped: A = Q shared); the group raster runs over cluster tiles
 template <bool SWAP, int MC>
 __device__ __forceinline__ void decode_ctile(int tile, int tiles_p, int tiles_q, uint32_t crank,
-                                             int& b, int& tp, int& tq) {
+                                             int& b, int& tp, int& tq, int gp = kGroupP) {
     if (MC == 1) {
-        decode_tile(tile, tiles_p, tiles_q, b, tp, tq);
+        decode_tile(tile, tiles_p, tiles_q, b, tp, tq, gp);
     } else if (!SWAP) {
-        decode_tile(tile, tiles_p, (tiles_q + MC - 1) / MC, b, tp, tq);
+        decode_tile(tile, tiles_p, (tiles_q + MC - 1) / MC, b, tp, tq, gp);
         tq = tq * MC + (int)crank;
     } else {
-        decode_tile(tile, (tiles_p + MC - 1) / MC, tiles_q, b, tp, tq);
+        decode_tile(tile, (tiles_p + MC - 1) / MC, tiles_q, b, tp, tq, gp);
         tp = tp * MC + (int)crank;
     }
 }
@@ -344,11 +345,45 @@ __device__ __forceinline__ void store_row_chunk(char* Cb, long long base, int n0
     }
 }
 
+// 16-bit rows that are 8-B but not 16-B aligned (N % 8 == 4, e.g. attention s = 1500):
+// 4-column uint2 stores per lane (its row), all-or-nothing per 4 columns (N % 4 == 0)
+template <int W>
+__device__ __forceinline__ void store_row_chunk8(char* Cb, long long base, int n0, int N,
+                                                 const float* f, int kind) {
+    uint32_t u[W / 2];
+    pack_chunk<W>(f, u, kind);
+    uint16_t* c = reinterpret_cast<uint16_t*>(Cb) + base + n0;
+#pragma unroll
+    for (int j = 0; j < W; j += 4)
+        if (n0 + j < N) *reinterpret_cast<uint2*>(c + j) = make_uint2(u[j / 2], u[j / 2 + 1]);
+}
+
 // scalar fallback (C rows not 16-B aligned or N % 8 != 0): rare, kept out of line
 __device__ __noinline__ void store_row_scalar(char* Cb, long long base, int n0, int N, int W,
                                               const float* f, int kind) {
     for (int j = 0; j < W; ++j)
         if (n0 + j < N) store1(Cb, base + n0 + j, f[j], kind);
+}
+
+// rows that are not 16-B aligned (N % 8 != 0, e.g. attention scores with s % 8 != 0, or a
+// ragged sequence): the warp transposes its 32 rows x W columns through its 4-KB staging
+// buffer (XOR-swizzled, conflict-free both ways), then writes row by row with consecutive
+// lanes on consecutive columns -- coalesced, instead of 32 lanes hitting 32 rows per store
+template <int W>
+__device__ __forceinline__ void store_rows_coalesced(float* st, char* Cb, long long ldc, int row0,
+                                                     int M, int n0, int N, const float* f,
+                                                     int kind, int lane) {
+#pragma unroll
+    for (int j = 0; j < W; ++j) st[lane * 32 + (j ^ lane)] = f[j];
+    __syncwarp();
+    const int col = n0 + lane;
+#pragma unroll 1
+    for (int r = 0; r < 32; ++r) {
+        const int row = row0 + r;
+        if (row >= M) break;                         // warp-uniform
+        if (lane < W && col < N) store1(Cb, (long long)row * ldc + col, st[r * 32 + (lane ^ r)], kind);
+    }
+    __syncwarp();
 }
 
 // transposed chunk (swap): lane owns output column `col`, registers are rows m0..m0+W-1
@@ -526,7 +561,7 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
                     int b_ = 0, tp_, tq_;
                     VarTile v_{0, 0, 0};
                     if (p.ngroups) decode_varlen<BN>(tile_, p.cu, p.ngroups, tp_, tq_, v_);
-                    else decode_ctile<SWAP, MC>(tile_, p.tiles_p, p.tiles_q, crank, b_, tp_, tq_);
+                    else decode_ctile<SWAP, MC>(tile_, p.tiles_p, p.tiles_q, crank, b_, tp_, tq_, p.group_p);
                     // this CTA's own rows (its half of a pair, its 1/MC share of the
                     // multicast operand): the maps' boxes are sized to them
                     const int pp = PAIR ? tp_ * 256 + (int)prank * 128
@@ -550,7 +585,7 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
                 int b = 0, tp, tq;
                 VarTile vt{0, 0, 0};   // varlen: the sequence's first packed row offsets P and Q
                 if (p.ngroups) decode_varlen<BN>(tile, p.cu, p.ngroups, tp, tq, vt);
-                else decode_ctile<SWAP, MC>(tile, p.tiles_p, p.tiles_q, crank, b, tp, tq);
+                else decode_ctile<SWAP, MC>(tile, p.tiles_p, p.tiles_q, crank, b, tp, tq, p.group_p);
                 if (pid == 0 && j == 0) cyc_at(p, 22, cy0);
                 for (int kb = k0; kb < k0 + nk; ++kb, ++j) {
                     // a unit is one k-block, or two (deep-K) when the next k-block of this
@@ -796,7 +831,7 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
             int b = 0, tp, tq;
             VarTile vt{0, 0, 0};
             if (p.ngroups) decode_varlen<BN>(tile, p.cu, p.ngroups, tp, tq, vt);
-            else decode_ctile<SWAP, MC>(tile, p.tiles_p, p.tiles_q, crank, b, tp, tq);
+            else decode_ctile<SWAP, MC>(tile, p.tiles_p, p.tiles_q, crank, b, tp, tq, p.group_p);
             // first P-axis row of this CTA's accumulator rows (a pair splits 256 rows)
             const int prow0 = PAIR ? tp * 256 + (int)prank * 128 : tp * 128;
             // ---- stream-K bookkeeping (before the accumulator wait) ---------------------
@@ -984,6 +1019,15 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
                 const float* f = reinterpret_cast<const float*>(v);
                 if (p.dbg & 8) {
                     if (f[0] == 12345.f) store1(Cb, 0, f[1], p.out_kind);
+                } else if (!SWAP && p.ndst == 0 && !vec_e && p.out_kind != 2 && (Ne & 3) == 0 &&
+                           ((reinterpret_cast<uintptr_t>(Cb) | (uintptr_t)(ldc_e * 2)) & 7) == 0) {
+                    if (pr < Me)
+                        store_row_chunk8<W>(Cb, (long long)pr * ldc_e, tq * BN + c * 32, Ne, f,
+                                            p.out_kind);
+                } else if (!SWAP && p.ndst == 0 && !vec_e) {
+                    store_rows_coalesced<W>(reinterpret_cast<float*>(sE + (warp - kEpiWarp0) * 4096),
+                                            Cb, ldc_e, prow0 + quarter * 32, Me, tq * BN + c * 32,
+                                            Ne, f, p.out_kind, lane);
                 } else if (!SWAP) {
                     // row pr = m, columns = n
                     if (pr < Me) {
@@ -1090,7 +1134,7 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
         cyr = clock64();
         if (warp >= kEpiWarp0 && warp < kEpiWarp0 + EW && !(p.dbg & 2)) {
             int b, tp, tq;
-            decode_tile(tile0, p.tiles_p, p.tiles_q, b, tp, tq);
+            decode_tile(tile0, p.tiles_p, p.tiles_q, b, tp, tq, p.group_p);
             const int et = threadIdx.x - kEpiWarp0 * 32;
             const float* red = reinterpret_cast<const float*>(sP);
             char* Cb = reinterpret_cast<char*>(p.C) +

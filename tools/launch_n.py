@@ -21,6 +21,7 @@ def main():
     M, N, K = int(a[0]), int(a[1]), int(a[2])
     force = (int(a[3]), int(a[4])) if len(a) > 4 else (-1, 0)
     p = vx.Plan(N, K, "bf16", out, "nk")
+    print("selected", p.select(M))
     A = synth.matrix((M, K), "bf16", seed=1, device="cuda")
     B = synth.matrix((N, K), "bf16", seed=2, scale=K ** -0.5, device="cuda")
     C = torch.empty((M, N), dtype={"bf16": torch.bfloat16, "fp32": torch.float32}[out], device="cuda")
