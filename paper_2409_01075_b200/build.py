@@ -16,8 +16,10 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libvx.so")
-SOURCES = ["vx_plan.cpp", "vx_calib.cpp", "vx_dispatch.cu", "vx_live.cu"]
-HEADERS = ["vx_internal.h", "vx_ptx.cuh", "vx_umma.cuh", "vx_simt.cuh", "vx_gemv.cuh"]
+SOURCES = ["vx_plan.cpp", "vx_calib.cpp", "vx_dispatch.cu", "vx_live.cu", "vx_k_single.cu",
+           "vx_k_swap.cu", "vx_k_pair.cu", "vx_k_mc.cu"]
+HEADERS = ["vx_internal.h", "vx_ptx.cuh", "vx_umma.cuh", "vx_simt.cuh", "vx_gemv.cuh",
+           "vx_kernels.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -35,13 +37,27 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
     tmp = LIB + ".tmp.%d" % os.getpid()
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
-           "-shared", "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"),
-           "-I", CSRC, "-o", tmp] + [os.path.join(CSRC, s) for s in SOURCES]
+    flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
+             "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"), "-I", CSRC]
     if verbose:
-        cmd += ["-Xptxas", "-v"]
-        print(" ".join(cmd), flush=True)
-    subprocess.check_call(cmd)
+        flags += ["-Xptxas", "-v"]
+    # one object per translation unit, compiled in parallel (the kernel instantiations are
+    # spread over vx_k_*.cu), then one shared-object link
+    objs, procs = [], []
+    for src in SOURCES:
+        obj = os.path.join(CSRC, ".obj", src + ".%d.o" % os.getpid())
+        os.makedirs(os.path.dirname(obj), exist_ok=True)
+        cmd = [NVCC, *flags, "-c", os.path.join(CSRC, src), "-o", obj]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        procs.append(subprocess.Popen(cmd))
+        objs.append(obj)
+    bad = [p.args for p in procs if p.wait() != 0]
+    if bad:
+        raise subprocess.CalledProcessError(1, bad[0])
+    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp] + objs)
+    for o in objs:
+        os.remove(o)
     os.replace(tmp, LIB)
     return LIB
 

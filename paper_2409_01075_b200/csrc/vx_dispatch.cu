@@ -14,7 +14,7 @@
 #include "vx_internal.h"
 #include "vx_gemv.cuh"
 #include "vx_simt.cuh"
-#include "vx_umma.cuh"
+#include "vx_kernels.h"
 
 namespace vx {
 
@@ -65,71 +65,13 @@ bool kernel_available(int family, int bm, int bn, int mc, int occ) {
     return false;
 }
 
-using UmmaFn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap,
-                        const CUtensorMap, const UmmaParams);
-
-template <int BN, bool SWAP>
-static UmmaFn pick_mn(bool b_mn) {
-    // B stored K x N makes B's tile MN-major: it is Q (non-swap) or P (swap)
-    if (SWAP) return b_mn ? (UmmaFn)vx_umma_kernel<BN, true, true, false>
-                          : (UmmaFn)vx_umma_kernel<BN, true, false, false>;
-    return b_mn ? (UmmaFn)vx_umma_kernel<BN, false, false, true>
-                : (UmmaFn)vx_umma_kernel<BN, false, false, false>;
-}
-
-template <int BN>
-static UmmaFn pick_pair(bool b_mn) {
-    return b_mn ? (UmmaFn)vx_umma_kernel<BN, false, false, true, true>
-                : (UmmaFn)vx_umma_kernel<BN, false, false, false, true>;
-}
-
-template <int BN, bool SWAP, int MC>
-static UmmaFn pick_mc(bool b_mn) {
-    if (SWAP) return b_mn ? (UmmaFn)vx_umma_kernel<BN, true, true, false, false, MC>
-                          : (UmmaFn)vx_umma_kernel<BN, true, false, false, false, MC>;
-    return b_mn ? (UmmaFn)vx_umma_kernel<BN, false, false, true, false, MC>
-                : (UmmaFn)vx_umma_kernel<BN, false, false, false, false, MC>;
-}
-
-
 static UmmaFn umma_fn(int family, int bm, int bn, bool b_mn, int mc = 1, int occ = 1) {
-    if (occ == 2) {
-        if (mc != 1 || !lean_available(family, bm, bn)) return nullptr;
-        return nullptr;   // no lean kernel instantiated (see lean_available)
-    }
-    if (mc > 1) {
-        if (!mc_available(family, bm, bn, mc)) return nullptr;
-        if (family == kUmma) return bn == 128 ? pick_mc<128, false, 2>(b_mn) : pick_mc<256, false, 2>(b_mn);
-        if (mc == 4) return pick_mc<64, true, 4>(b_mn);
-        return bn == 32 ? pick_mc<32, true, 2>(b_mn) : pick_mc<64, true, 2>(b_mn);
-    }
-    if (family == kUmma && bm == 256) {
-        switch (bn) {
-        case 64:   // each CTA holds 32 B rows: K-major B only (an MN-major 128-B swizzle
-                   // atom is 64 elements wide), vx_plan keeps this rung for VX_B_NK only
-            return b_mn ? nullptr : (UmmaFn)vx_umma_kernel<64, false, false, false, true>;
-        case 128: return pick_pair<128>(b_mn);
-        case 256: return pick_pair<256>(b_mn);
-        }
-        return nullptr;
-    }
-    if (family == kUmma) {
-        switch (bn) {
-        case 64: return pick_mn<64, false>(b_mn);
-        case 128: return pick_mn<128, false>(b_mn);
-        case 192: return pick_mn<192, false>(b_mn);
-        case 256: return pick_mn<256, false>(b_mn);
-        }
-    } else if (family == kUmmaSwap) {
-        switch (bn) {
-        case 16: return pick_mn<16, true>(b_mn);
-        case 32: return pick_mn<32, true>(b_mn);
-        case 64: return pick_mn<64, true>(b_mn);
-        case 128: return pick_mn<128, true>(b_mn);
-        case 192: return pick_mn<192, true>(b_mn);
-        case 256: return pick_mn<256, true>(b_mn);
-        }
-    }
+    if (occ == 2) return nullptr;   // no lean kernel instantiated (see lean_available)
+    if (mc > 1) return mc_available(family, bm, bn, mc) ? umma_fn_mc(family, bn, mc, b_mn) : nullptr;
+    if (!kernel_available(family, bm, bn, 1, 1)) return nullptr;
+    if (family == kUmma && bm == 256) return umma_fn_pair(bn, b_mn);
+    if (family == kUmma) return umma_fn_single(bn, b_mn);
+    if (family == kUmmaSwap) return umma_fn_swap(bn, b_mn);
     return nullptr;
 }
 

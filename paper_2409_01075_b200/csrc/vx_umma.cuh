@@ -359,7 +359,7 @@ __device__ __forceinline__ void store_row_chunk8(char* Cb, long long base, int n
 }
 
 // scalar fallback (C rows not 16-B aligned or N % 8 != 0): rare, kept out of line
-__device__ __noinline__ void store_row_scalar(char* Cb, long long base, int n0, int N, int W,
+static __device__ __noinline__ void store_row_scalar(char* Cb, long long base, int n0, int N, int W,
                                               const float* f, int kind) {
     for (int j = 0; j < W; ++j)
         if (n0 + j < N) store1(Cb, base + n0 + j, f[j], kind);

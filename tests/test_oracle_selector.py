@@ -192,6 +192,6 @@ def test_streamk_only_for_few_waves():
     assert not S.streamk_admissible(big, 1, 16384, 11008, 4096, DESC)
     assert S.streamk_admissible(big, 1, 512, 11008, 4096, DESC)
     # few k-blocks per CTA (BERT-size K, many small tiles): a tile would be cut over > 3 CTAs
-    sw16 = [r for r in t["rungs"] if r["family"] == 1 and r["bn"] == 16][0]
+    sw16 = [r for r in t["rungs"] if r["family"] == 1 and r["bm"] == 128 and r["bn"] == 16][0]
     assert not S.streamk_admissible(sw16, 1, 32, 2304, 768, DESC)
     assert S.streamk_admissible(sw16, 1, 4, 11008, 4096, DESC)
