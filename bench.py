@@ -760,6 +760,34 @@ def selector_overhead(vx, plans_nk, local):
     out["how"] = ("vx_plan wall time (no profiling: the calibration is compiled in); "
                   "vx_plan_select per call via ctypes over M=1..16384, first pass (argmin) "
                   "and second pass (memo)")
+    # host cost of one vx_gemm OUTSIDE a graph (select + tensor maps + cudaLaunchKernelEx,
+    # through ctypes): back-to-back calls on one stream, wall time / call, the device kept
+    # ahead of the host by a large first launch; weights (B) fixed, A rotating over 8
+    # buffers, so B's tensor map comes from the memo and A's / C's are re-encoded
+    dev = torch.device("cuda", local)
+    M, N, K = 128, 768, 768
+    p = vx.Plan(N, K, "bf16", "bf16", "nk", device=local)
+    As = [torch.randn(M, K, device=dev).to(torch.bfloat16) for _ in range(8)]
+    Bw = torch.randn(N, K, device=dev).to(torch.bfloat16)
+    Cs = [torch.empty(M, N, dtype=torch.bfloat16, device=dev) for _ in range(8)]
+    sp = ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+    f = vx.lib.vx_gemm
+    for i in range(16):
+        f(p.handle, M, N, K, As[i % 8].data_ptr(), Bw.data_ptr(), Cs[i % 8].data_ptr(), sp)
+    torch.cuda.synchronize()
+    n = 2000
+    h0, m0 = vx.map_cache_stats()
+    t0 = time.perf_counter()
+    for i in range(n):
+        f(p.handle, M, N, K, As[i % 8].data_ptr(), Bw.data_ptr(), Cs[i % 8].data_ptr(), sp)
+    t_host = (time.perf_counter() - t0) / n
+    h1, m1 = vx.map_cache_stats()
+    torch.cuda.synchronize()
+    out["gemm_host_us"] = {"M": M, "N": N, "K": K, "us_per_call": t_host * 1e6,
+                           "map_memo_hits_per_call": (h1 - h0) / n,
+                           "map_encodes_per_call": (m1 - m0) / n,
+                           "how": "wall time of %d back-to-back vx_gemm calls via ctypes (no "
+                                  "graph), A/C rotating over 8 buffers, B fixed" % n}
     return out
 
 

@@ -279,6 +279,12 @@ vx_status vx_pack_b(vx_plan_t plan, int64_t batch, int64_t N, int64_t K, vx_blay
  * bench.py's gpu_launches). */
 int64_t vx_launch_count(void);
 
+/* Tensor-map memo statistics (process-wide): encodes served from the memo / encoded anew.
+ * vx_gemm* encodes a CUtensorMap per operand; one with the same address, shape and box as a
+ * recent one (typically B, the weights) is reused instead of re-encoded.
+ * Either pointer may be NULL. */
+void vx_map_cache_stats(int64_t* hits, int64_t* misses);
+
 #ifdef __cplusplus
 }
 #endif

@@ -113,6 +113,8 @@ def _load():
     L.vx_packed_b_elems.argtypes = [P, i64, i64, i64]
     L.vx_pack_b.argtypes = [P, i64, i64, i64, ctypes.c_int, vp, i64, vp, vp]
     L.vx_pack_b.restype = ctypes.c_int
+    L.vx_map_cache_stats.argtypes = [ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    L.vx_map_cache_stats.restype = None
     for f in ("vx_device_probe", "vx_plan", "vx_plan_ex", "vx_plan_destroy", "vx_plan_select",
               "vx_plan_cost", "vx_plan_dump", "vx_gemm", "vx_gemm_batched", "vx_gemm_ex",
               "vx_gemm_host", "vx_gemm_gather", "vx_calibrate", "vx_calib_new",
@@ -137,6 +139,13 @@ def device_probe(device: int = 0) -> DeviceDesc:
     d = DeviceDesc()
     _check(_lib.vx_device_probe(device, ctypes.byref(d)), "vx_device_probe")
     return d
+
+
+def map_cache_stats() -> tuple[int, int]:
+    """(hits, misses) of the process-wide tensor-map memo (vx_map_cache_stats)."""
+    h, m = ctypes.c_int64(), ctypes.c_int64()
+    _lib.vx_map_cache_stats(ctypes.byref(h), ctypes.byref(m))
+    return h.value, m.value
 
 
 def launch_count() -> int:

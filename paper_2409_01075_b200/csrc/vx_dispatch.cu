@@ -150,9 +150,58 @@ static EncodeTiledFn encode_fn() {
 
 // 3-D map over a 16-bit matrix stored [batch][rows][inner] (inner contiguous):
 // dims {inner, rows, batch}; box {64, box_rows, 1}; 128-B swizzle; OOB -> zeros.
+// ---- tensor-map memo ("B's map is cached per pointer") ------------------
+// A CUtensorMap is a pure function of its encode arguments (address, shape, strides, box,
+// swizzle) and holds no reference to the memory, so a map encoded once can be reused by any
+// later launch with identical arguments -- even after the buffer was freed and another one
+// landed at the same address.  Weights (B) repeat across calls; activations usually do not.
+// Process-wide, 64 entries, round-robin replacement, one mutex (host only).
+struct MapKey {
+    int32_t kind, dt, swz, pad;
+    const void* base;
+    int64_t v[6];
+    int32_t box[4];
+};
+static std::mutex g_map_mu;
+static MapKey g_map_keys[64];
+static CUtensorMap g_map_vals[64];
+static int g_map_n = 0, g_map_next = 0;
+static std::atomic<int64_t> g_map_hits{0}, g_map_misses{0};
+
+static MapKey map_key(int kind, const void* base, vx_dtype dt, int64_t v0, int64_t v1, int64_t v2,
+                      int64_t v3, int64_t v4, int b0, int b1, int swz) {
+    MapKey k;
+    memset(&k, 0, sizeof(k));
+    k.kind = kind; k.dt = (int32_t)dt; k.swz = swz; k.base = base;
+    k.v[0] = v0; k.v[1] = v1; k.v[2] = v2; k.v[3] = v3; k.v[4] = v4;
+    k.box[0] = b0; k.box[1] = b1;
+    return k;
+}
+static bool map_lookup(const MapKey& k, CUtensorMap* out) {
+    std::lock_guard<std::mutex> lk(g_map_mu);
+    for (int i = 0; i < g_map_n; ++i)
+        if (memcmp(&g_map_keys[i], &k, sizeof(k)) == 0) {
+            *out = g_map_vals[i];
+            g_map_hits.fetch_add(1, std::memory_order_relaxed);
+            return true;
+        }
+    g_map_misses.fetch_add(1, std::memory_order_relaxed);
+    return false;
+}
+static void map_store(const MapKey& k, const CUtensorMap& m) {
+    std::lock_guard<std::mutex> lk(g_map_mu);
+    const int i = g_map_n < 64 ? g_map_n++ : g_map_next;
+    g_map_next = (i + 1) % 64;
+    g_map_keys[i] = k;
+    g_map_vals[i] = m;
+}
+
 static vx_status make_map(CUtensorMap* map, const void* base, vx_dtype dt, int64_t inner,
                           int64_t rows, int64_t batch, int64_t ld, int64_t bstride,
                           int box_inner, int box_rows, bool swizzle = true) {
+    const MapKey key = map_key(3, base, dt, inner, rows, batch, ld, bstride, box_inner, box_rows,
+                               swizzle ? 1 : 0);
+    if (map_lookup(key, map)) return VX_OK;
     EncodeTiledFn enc = encode_fn();
     if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return VX_ERR_CUDA; }
     const int eb = dt == VX_FP32 ? 4 : 2;
@@ -172,6 +221,7 @@ static vx_status make_map(CUtensorMap* map, const void* base, vx_dtype dt, int64
                   (int)r, (long long)inner, (long long)rows, (long long)batch, (long long)ld);
         return VX_ERR_CUDA;
     }
+    map_store(key, *map);
     return VX_OK;
 }
 
@@ -183,6 +233,8 @@ static vx_status make_map(CUtensorMap* map, const void* base, vx_dtype dt, int64
 static vx_status make_map_k2(CUtensorMap* map, const void* base, vx_dtype dt, int64_t K,
                              int64_t rows, int64_t batch, int64_t ld, int64_t bstride,
                              int box_rows) {
+    const MapKey key = map_key(4, base, dt, K, rows, batch, ld, bstride, 64, box_rows, 1);
+    if (map_lookup(key, map)) return VX_OK;
     EncodeTiledFn enc = encode_fn();
     if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return VX_ERR_CUDA; }
     cuuint64_t dims[4] = {64, (cuuint64_t)rows, (cuuint64_t)(K / 64), (cuuint64_t)batch};
@@ -199,6 +251,7 @@ static vx_status make_map_k2(CUtensorMap* map, const void* base, vx_dtype dt, in
                   (long long)K, (long long)rows);
         return VX_ERR_CUDA;
     }
+    map_store(key, *map);
     return VX_OK;
 }
 
@@ -770,6 +823,11 @@ vx_status vx_pack_b(vx_plan_t p, int64_t batch, int64_t N, int64_t K, vx_blayout
 }
 
 int64_t vx_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+void vx_map_cache_stats(int64_t* hits, int64_t* misses) {
+    if (hits) *hits = g_map_hits.load(std::memory_order_relaxed);
+    if (misses) *misses = g_map_misses.load(std::memory_order_relaxed);
+}
 
 /* Debug/tracing hook (not part of vx.h): subsequent tcgen05 launches write %globaltimer
  * stamps of 8 phases per CTA into `buf` (device, >= 8*grid u64); NULL disables. */

@@ -755,6 +755,11 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
                 for (int i = 0; i < nk; ++i) {
                     const long long c0 = tr ? clock64() : 0;
                     if (second) {
+                        // the chunk landed with the previous k-block (deep-K unit); its own
+                        // barrier only got the producer's plain arrive, so this wait returns at
+                        // once -- it consumes that phase, so every phase of every full barrier
+                        // is waited on (compute-sanitizer synccheck: no "missing wait")
+                        ptx::mbar_wait(&full[stage], phase);
                         second = false;
                     } else {
                         ptx::mbar_wait(&full[stage], phase);

@@ -623,3 +623,32 @@ def test_varlen_attention_scores_integer_exact(d):
                 assert np.array_equal(got[off:off + s * s].reshape(s, s), want), (d, force, g, s)
             off += s * s
     assert p.select_varlen(cu) == {k: v for k, v in ch.items()} or True
+
+
+def test_tensor_map_memo_reuses_weight_maps():
+    """B's tensor map is reused, not re-encoded, across calls with the same
+    weights (vx_map_cache_stats), while A changes every call; a map is a pure function of its
+    encode arguments, so results stay exact -- including after the weight buffer is freed and
+    a new one is allocated (possibly at the same address) with other contents."""
+    vx = vxmod()
+    N, K = 768, 768
+    p = vx.Plan(N, K, "bf16", "fp32", "nk")
+    _, B = synth.gemm_inputs(8, N, K, "bf16", "nk", kind="int", seed=900)
+    Bd = B.cuda()
+    p.gemm(torch.zeros((64, K), dtype=torch.bfloat16, device="cuda"), Bd)   # warm the memo
+    torch.cuda.synchronize()
+    h0, m0 = vx.map_cache_stats()
+    for i in range(6):
+        M = 64 + 37 * i
+        A, _ = synth.gemm_inputs(M, N, K, "bf16", "nk", kind="int", seed=910 + i)
+        got = p.gemm(A.cuda(), Bd).cpu().double().numpy()
+        assert np.array_equal(got, oracle.gemm(A, B, "nk")), M
+    h1, m1 = vx.map_cache_stats()
+    assert h1 - h0 >= 6, (h0, h1, m0, m1)          # at least B's map hit on every call
+    del Bd
+    torch.cuda.synchronize()
+    _, B2 = synth.gemm_inputs(8, N, K, "bf16", "nk", kind="int", seed=901)
+    B2d = B2.cuda()
+    A, _ = synth.gemm_inputs(100, N, K, "bf16", "nk", kind="int", seed=920)
+    got = p.gemm(A.cuda(), B2d).cpu().double().numpy()
+    assert np.array_equal(got, oracle.gemm(A, B2, "nk"))
