@@ -52,12 +52,15 @@ def build(force: bool = False, verbose: bool = False) -> str:
             print(" ".join(cmd), flush=True)
         procs.append(subprocess.Popen(cmd))
         objs.append(obj)
-    bad = [p.args for p in procs if p.wait() != 0]
-    if bad:
-        raise subprocess.CalledProcessError(1, bad[0])
-    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp] + objs)
-    for o in objs:
-        os.remove(o)
+    try:
+        bad = [p.args for p in procs if p.wait() != 0]
+        if bad:
+            raise subprocess.CalledProcessError(1, bad[0])
+        subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp] + objs)
+    finally:
+        for o in objs:
+            if os.path.exists(o):
+                os.remove(o)
     os.replace(tmp, LIB)
     return LIB
 

@@ -173,3 +173,39 @@ class ShardedGemm:
                 raise ValueError("A shard has %d rows, expected %d" % (A.shape[0], hi - lo))
         c = self.local_gemm(A, B)
         return gather_rows(c, M, self.group) if gather else c
+
+
+class ShardedBatchedGemm:
+    """Batched attention scores S_b = Q_b x K_b^T (BASELINE configs[3]) sharded over the
+    BATCH: rank r computes batches row_shard(batch, world, r) with its own vx_gemm_batched
+    ("batched attention shards over batch (32/P) the same way").  Batches are
+    independent -- no reduction; a gathered S (all batches on every rank) is one
+    all_gather_into_tensor of the per-rank [b_r, s, s] blocks, padded to the largest.
+
+    local_bgemm(Q [b, s, d], Kt [b, s, d]) -> S [b, s, s] runs on this rank's device; by
+    default the library's batched Plan.gemm (Plan(s, d, ..., "nk"): K stored N x K)."""
+
+    def __init__(self, s: int, d: int, group=None, local_bgemm: Callable | None = None,
+                 in_dtype: str = "bf16", out_dtype: str = "bf16", device: int | None = None):
+        import torch.distributed as dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        if local_bgemm is None:
+            from . import Plan
+            plan = Plan(s, d, in_dtype, out_dtype, "nk",
+                        device=device if device is not None else torch.cuda.current_device())
+            local_bgemm = lambda q, k: plan.gemm(q, k)  # noqa: E731
+        self.local_bgemm = local_bgemm
+
+    def forward(self, Q: torch.Tensor, Kt: torch.Tensor, gather: bool = False) -> torch.Tensor:
+        """Q, Kt: the FULL [batch, s, d] inputs (each rank slices its batches).  Returns this
+        rank's [b_r, s, s] scores, or all [batch, s, s] if gather=True."""
+        batch = Q.shape[0]
+        lo, hi = row_shard(batch, self.world, self.rank)
+        S = self.local_bgemm(Q[lo:hi].contiguous(), Kt[lo:hi].contiguous())
+        if not gather:
+            return S
+        b_r, s1, s2 = S.shape
+        full = gather_rows(S.reshape(b_r, s1 * s2), batch, self.group)
+        return full.reshape(batch, s1, s2)

@@ -13,8 +13,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2409_01075_b200.dist import (ShardedGemm, gather_plan, gather_rows, push_rows,
-                                        row_shard, shard_sizes)
+from paper_2409_01075_b200.dist import (ShardedBatchedGemm, ShardedGemm, gather_plan,
+                                        gather_rows, push_rows, row_shard, shard_sizes)
 
 
 def test_row_shard_partition_properties():
@@ -102,3 +102,55 @@ def test_gather_plan_covers_every_destination_once():
                 for d in gp["dst_ranks"]:
                     hits[d, lo:hi] += 1
             assert (hits == 1).all()
+
+
+def _batched_worker(rank, world, port, batch, s, d, q):
+    import oracle
+    import synth
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        Q = synth.matrix((batch, s, d), "fp32", "int", seed=11)
+        Kt = synth.matrix((batch, s, d), "fp32", "int", seed=12)
+
+        def bgemm(q_, k_):        # injected local batched GEMM: the fp64 oracle per batch
+            return torch.stack([torch.from_numpy(oracle.gemm(q_[b], k_[b], "nk")).float()
+                                for b in range(q_.shape[0])]) if q_.shape[0] else \
+                torch.zeros((0, s, s))
+        sh = ShardedBatchedGemm(s, d, local_bgemm=bgemm)
+        lo, hi = row_shard(batch, world, rank)
+        mine = sh.forward(Q, Kt)
+        full = sh.forward(Q, Kt, gather=True)
+        q.put((rank, lo, hi, mine.numpy(), full.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,batch", [(2, 32), (3, 32), (2, 3)])
+def test_batch_sharded_attention_equals_full(world, batch):
+    """batched attention scores shard over the batch; every rank's block and the
+    gathered S equal the unsharded per-batch products (integer inputs: exact)."""
+    import oracle
+    import synth
+    s, d = 9, 16
+    ctx = mp.get_context("spawn")
+    qu = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_batched_worker, args=(r, world, port, batch, s, d, qu))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [qu.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    Q = synth.matrix((batch, s, d), "fp32", "int", seed=11)
+    Kt = synth.matrix((batch, s, d), "fp32", "int", seed=12)
+    want = np.stack([oracle.gemm(Q[b], Kt[b], "nk") for b in range(batch)])
+    covered = np.zeros(batch, dtype=int)
+    for rank, lo, hi, mine, full in res:
+        assert np.array_equal(mine, want[lo:hi])
+        assert np.array_equal(full, want)
+        covered[lo:hi] += 1
+    assert (covered == 1).all()
