@@ -4,10 +4,12 @@
 namespace vx {
 template <int BN, bool SWAP, int MC>
 static UmmaFn pick_mc(bool b_mn) {
-    if (SWAP) return b_mn ? (UmmaFn)vx_umma_kernel<BN, true, true, false, false, MC>
-                          : (UmmaFn)vx_umma_kernel<BN, true, false, false, false, MC>;
-    return b_mn ? (UmmaFn)vx_umma_kernel<BN, false, false, true, false, MC>
-                : (UmmaFn)vx_umma_kernel<BN, false, false, false, false, MC>;
+    if constexpr (SWAP)
+        return b_mn ? (UmmaFn)vx_umma_kernel<BN, true, true, false, false, MC>
+                    : (UmmaFn)vx_umma_kernel<BN, true, false, false, false, MC>;
+    else
+        return b_mn ? (UmmaFn)vx_umma_kernel<BN, false, false, true, false, MC>
+                    : (UmmaFn)vx_umma_kernel<BN, false, false, false, false, MC>;
 }
 
 UmmaFn umma_fn_mc(int family, int bn, int mc, bool b_mn) {

@@ -17,10 +17,12 @@ UmmaFn umma_fn_mc(int family, int bn, int mc, bool b_mn);   // TMA-multicast clu
 // B stored K x N makes B's tile MN-major: it is Q (non-swap) or P (swap)
 template <int BN, bool SWAP>
 UmmaFn pick_mn(bool b_mn) {
-    if (SWAP) return b_mn ? (UmmaFn)vx_umma_kernel<BN, true, true, false>
-                          : (UmmaFn)vx_umma_kernel<BN, true, false, false>;
-    return b_mn ? (UmmaFn)vx_umma_kernel<BN, false, false, true>
-                : (UmmaFn)vx_umma_kernel<BN, false, false, false>;
+    if constexpr (SWAP)
+        return b_mn ? (UmmaFn)vx_umma_kernel<BN, true, true, false>
+                    : (UmmaFn)vx_umma_kernel<BN, true, false, false>;
+    else
+        return b_mn ? (UmmaFn)vx_umma_kernel<BN, false, false, true>
+                    : (UmmaFn)vx_umma_kernel<BN, false, false, false>;
 }
 
 }  // namespace vx

@@ -167,7 +167,7 @@ __device__ __forceinline__ void epi_bar() {   // named barrier over the epilogue
     asm volatile("bar.sync 1, %0;" ::"n"(ET) : "memory");
 }
 
-constexpr int kTraceSlots = 40;
+constexpr int kTraceSlots = 56;   // 40-47: issue cycle of units 0-7, 48-55: their full-barrier wait exit
 // phase trace (tracing aux subsystem): %globaltimer (ns) at fixed points, 20 slots per CTA
 // (slots 12-15: MMA-issuer cycle counters, see the MMA loop)
 __device__ __forceinline__ void trace_at(const UmmaParams& p, int slot) {
@@ -552,12 +552,14 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
             bool stamped = pid != 0;
             bool waited = false;
             int j = 0;                       // running k-block count of this CTA
-            // first k-block of this producer: (pid 0) L2 prefetch of the CTA's first ring of
-            // P and Q tiles -- the loads after the wait then hit L2 -- then the grid
-            // dependency wait (no global memory is touched before it)
+            // first k-block of this producer: the grid dependency wait (no global memory is
+            // touched before it).  An L2 prefetch of the CTA's first ring before the wait
+            // (VX_DEBUG_FLAGS 128 turns it back on, A/B only) was measured to DELAY the real
+            // loads -- the prefetches occupy the CTA's TMA queue ahead of them: BERT-size
+            // launches 5.9 -> 5.1 us without it
             auto dep_wait = [&](int tile_, int kb_, int nleft) {
                 if (waited) return;
-                if (pid == 0 && !(p.dbg & 128) && !p.bpack && !P_MN && !Q_MN) {
+                if (pid == 0 && (p.dbg & 128) && !p.bpack && !P_MN && !Q_MN) {
                     int b_ = 0, tp_, tq_;
                     VarTile v_{0, 0, 0};
                     if (p.ngroups) decode_varlen<BN>(tile_, p.cu, p.ngroups, tp_, tq_, v_);
@@ -600,6 +602,7 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
                     if (dbl) ptx::mbar_wait(&empty[stage + 1], phase ^ 1);
                     if (j == 0) cyc_at(p, 23, cy0);
+                    if (j < 8) cyc_at(p, 40 + j, cyc_entry);
                     if (kb >= k0 + PW && !stamped) { trace_at(p, 10); stamped = true; }
                     uint8_t* dP = sP + stage * kP;
                     uint8_t* dQ = sQ + stage * kQ;
@@ -751,50 +754,59 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
                 ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
                 ptx::tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
-                bool second = false;   // this k-block landed with the previous one (deep-K unit)
-                for (int i = 0; i < nk; ++i) {
+                // one iteration per unit: a k-block, or a deep-K pair of k-blocks that landed
+                // together on full[stage] (the producers' rule) -- one wait, 4 or 8 MMAs, one
+                // commit per stage.  The second stage's barrier only got the producer's plain
+                // arrive; its phase completes without a waiter, which keeps every barrier at
+                // one completion per ring round, so the parity this loop tracks stays exact.
+                // (Per-unit MMA-warp time is what bounds small tiles: DESIGN.md 4.4.)
+                int nunit = 0;   // trace: units of the first tile
+                for (int i = 0; i < nk;) {
+                    const bool dbl = kd && i + 1 < nk && stage + 1 < S;
                     const long long c0 = tr ? clock64() : 0;
-                    if (second) {
-                        // the chunk landed with the previous k-block (deep-K unit); its own
-                        // barrier only got the producer's plain arrive, so this wait returns at
-                        // once -- it consumes that phase, so every phase of every full barrier
-                        // is waited on (compute-sanitizer synccheck: no "missing wait")
-                        ptx::mbar_wait(&full[stage], phase);
-                        second = false;
-                    } else {
-                        ptx::mbar_wait(&full[stage], phase);
-                        ptx::tc_fence_after();
-                        second = kd && i + 1 < nk && stage + 1 < S;   // producers' rule
-                    }
+                    ptx::mbar_wait(&full[stage], phase);
+                    ptx::tc_fence_after();
                     const long long c1 = tr ? clock64() : 0;
                     if (it == 0 && i == 0 && lane == 0) trace_at(p, 3);
+                    if (tr && it == 0 && lane == 0 && nunit < 8) cyc_at(p, 48 + nunit, cyc_entry);
+                    ++nunit;
                     const uint64_t dp0 = dP_base + (uint64_t)(stage * (kP >> 4));
                     const uint64_t dq0 = dQ_base + (uint64_t)(stage * (kQ >> 4));
                     long long c2 = 0;
                     if (ptx::elect_one()) {
                         if (!mma_off) {
 #pragma unroll
-                            for (int k = 0; k < 4; ++k) {
-                                // K-major: +32 B inside the swizzle row; MN-major: +2 K-groups
-                                const uint64_t dp = dp0 + k * kStepP;
-                                const uint64_t dq = dq0 + k * kStepQ;
+                            for (int k = 0; k < 8; ++k) {
+                                if (k >= 4 && !dbl) break;
+                                // K-major: +32 B inside the swizzle row; MN-major: +2 K-groups;
+                                // chunks 4..7 read the next stage (+ one P / Q tile)
+                                const uint64_t dp = dp0 + (k >> 2) * (kP >> 4) + (k & 3) * kStepP;
+                                const uint64_t dq = dq0 + (k >> 2) * (kQ >> 4) + (k & 3) * kStepQ;
                                 if (PAIR) ptx::umma_f16_pair(d_tmem, dp, dq, idesc, (i | k) != 0);
                                 else ptx::umma_f16(d_tmem, dp, dq, idesc, (i | k) != 0);
                             }
                         }
                         c2 = tr ? clock64() : 0;
-                        // frees the stage (in both CTAs of a pair / every CTA of a multicast
-                        // cluster) when these MMAs finish
+                        // frees the stage(s) (in both CTAs of a pair / every CTA of a
+                        // multicast cluster) when these MMAs finish
                         if (PAIR) ptx::umma_commit_pair(&empty[stage], 3);
                         else if (MC > 1) ptx::umma_commit_mc(&empty[stage], kMcMask);
                         else ptx::umma_commit(&empty[stage]);
+                        if (dbl) {
+                            if (PAIR) ptx::umma_commit_pair(&empty[stage + 1], 3);
+                            else if (MC > 1) ptx::umma_commit_mc(&empty[stage + 1], kMcMask);
+                            else ptx::umma_commit(&empty[stage + 1]);
+                        }
                         if (tr) {
                             const long long c3 = clock64();
                             cyc_wait += c1 - c0; cyc_mma += c2 - c1; cyc_commit += c3 - c2; ++cyc_n;
                         }
                     }
                     __syncwarp();
-                    if (++stage == S) { stage = 0; phase ^= 1; }
+                    const int adv = dbl ? 2 : 1;
+                    i += adv;
+                    stage += adv;
+                    if (stage == S) { stage = 0; phase ^= 1; }
                 }
                 // accumulator ready for the epilogue (of both CTAs of a pair)
                 if (ptx::elect_one()) {

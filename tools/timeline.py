@@ -20,7 +20,7 @@ import synth
 
 PH = ["entry", "setup", "prod_done", "first_full", "mma_done", "acc_ready", "epi_done",
       "pre_teardown", "dep_released", "exit", "2nd_issue", "1st_issue", "-", "-", "-", "-", "split_sync1", "split_posted", "-", "-"] + ["-"] * 20
-NS = 40   # slots per CTA; 12-15 = MMA-issuer cycle counters (wait, issue, commit, n), 18-31 cycle stamps
+NS = 56   # slots per CTA; 12-15 = MMA-issuer cycle counters (wait, issue, commit, n), 18-31 cycle stamps
 
 
 def main():
@@ -107,6 +107,17 @@ def main():
         c = c[c > 0]
         if len(c):
             print("  cyc %-30s median %7.0f  max %7.0f" % (nm, np.median(c), c.max()))
+    iss = t[1:, :, 40:48].reshape(-1, 8).astype(float)
+    arr = t[1:, :, 48:56].reshape(-1, 8).astype(float)
+    if (iss[:, 0] > 0).any():
+        dep = t[1:, :, 27].reshape(-1).astype(float)       # dependency released (entry+)
+        ok = iss[:, 0] > 0
+        print("  units 0-7, cycles after the dependency release (median over CTAs):")
+        print("    issued  " + " ".join("%6.0f" % np.median(iss[ok, u] - dep[ok]) for u in range(8)
+                                       if (iss[ok, u] > 0).any()))
+        ok2 = arr[:, 0] > 0
+        print("    landed  " + " ".join("%6.0f" % np.median(arr[ok2, u] - dep[ok2]) for u in range(8)
+                                       if (arr[ok2, u] > 0).any()))
     for nm in PH:
         if nm != "-" and rows[nm]:
             v = np.median(np.array(rows[nm]), axis=0)
