@@ -350,9 +350,20 @@ vx_status launch(const vx_plan_s* p, const vx_choice& ch, int64_t batch, int64_t
         if (!fn) { set_error("no SIMT kernel %dx%d", r.bm, r.bn); return VX_ERR_UNSUPPORTED; }
         const int tm = (int)cdiv(M, r.bm), tn = (int)cdiv(N, r.bn);
         const int64_t grid = batch * (int64_t)tm * tn;
-        fn<<<(unsigned)grid, threads, 0, st>>>((const float*)A, (const float*)B, (float*)C, (int)M,
-                                               (int)N, (int)K, p->bl == VX_B_NK, sA, sB, sC, tm, tn);
-        cudaError_t e = cudaGetLastError();
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)grid, 1, 1);
+        cfg.blockDim = dim3((unsigned)threads, 1, 1);
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        if (g_pdl) {   // the kernel waits (griddepcontrol.wait) before its first global access
+            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+        }
+        cudaError_t e = cudaLaunchKernelEx(&cfg, fn, (const float*)A, (const float*)B, (float*)C,
+                                           (int)M, (int)N, (int)K, (int)(p->bl == VX_B_NK),
+                                           (long long)sA, (long long)sB, (long long)sC, tm, tn);
         if (e != cudaSuccess) return cuda_fail(e, "SIMT launch");
         g_launches.fetch_add(1, std::memory_order_relaxed);
         return VX_OK;

@@ -345,19 +345,6 @@ __device__ __forceinline__ void store_row_chunk(char* Cb, long long base, int n0
     }
 }
 
-// 16-bit rows that are 8-B but not 16-B aligned (N % 8 == 4, e.g. attention s = 1500):
-// 4-column uint2 stores per lane (its row), all-or-nothing per 4 columns (N % 4 == 0)
-template <int W>
-__device__ __forceinline__ void store_row_chunk8(char* Cb, long long base, int n0, int N,
-                                                 const float* f, int kind) {
-    uint32_t u[W / 2];
-    pack_chunk<W>(f, u, kind);
-    uint16_t* c = reinterpret_cast<uint16_t*>(Cb) + base + n0;
-#pragma unroll
-    for (int j = 0; j < W; j += 4)
-        if (n0 + j < N) *reinterpret_cast<uint2*>(c + j) = make_uint2(u[j / 2], u[j / 2 + 1]);
-}
-
 // scalar fallback (C rows not 16-B aligned or N % 8 != 0): rare, kept out of line
 static __device__ __noinline__ void store_row_scalar(char* Cb, long long base, int n0, int N, int W,
                                               const float* f, int kind) {
@@ -382,6 +369,34 @@ __device__ __forceinline__ void store_rows_coalesced(float* st, char* Cb, long l
         const int row = row0 + r;
         if (row >= M) break;                         // warp-uniform
         if (lane < W && col < N) store1(Cb, (long long)row * ldc + col, st[r * 32 + (lane ^ r)], kind);
+    }
+    __syncwarp();
+}
+
+// 16-bit rows that are 8-B but not 16-B aligned (N % 8 == 4, e.g. attention s = 100, 1500):
+// the warp transposes its 32 rows x W columns through its staging buffer as above, then each
+// store instruction covers 4 rows x 32 columns with one 8-B (4-column) store per lane, so a
+// row's W columns leave as one contiguous 64-B segment -- instead of 32 lanes each writing 8 B
+// into 32 different rows (N % 4 == 0: 4 columns are all-or-nothing)
+template <int W>
+__device__ __forceinline__ void store_rows_coalesced8(float* st, char* Cb, long long ldc, int row0,
+                                                      int M, int n0, int N, const float* f,
+                                                      int kind, int lane) {
+#pragma unroll
+    for (int j = 0; j < W; ++j) st[lane * 32 + (j ^ lane)] = f[j];
+    __syncwarp();
+    const int c = (lane & 7) * 4;
+#pragma unroll 1
+    for (int it = 0; it < 8; ++it) {
+        const int r = it * 4 + (lane >> 3);
+        const int row = row0 + r;
+        if (row < M && c < W && n0 + c < N) {
+            const float* sr = st + r * 32;
+            const uint32_t lo = pack2(sr[c ^ r], sr[(c + 1) ^ r], kind);
+            const uint32_t hi = pack2(sr[(c + 2) ^ r], sr[(c + 3) ^ r], kind);
+            *reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(Cb) + (long long)row * ldc + n0 + c) =
+                make_uint2(lo, hi);
+        }
     }
     __syncwarp();
 }
@@ -1038,9 +1053,9 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
                     if (f[0] == 12345.f) store1(Cb, 0, f[1], p.out_kind);
                 } else if (!SWAP && p.ndst == 0 && !vec_e && p.out_kind != 2 && (Ne & 3) == 0 &&
                            ((reinterpret_cast<uintptr_t>(Cb) | (uintptr_t)(ldc_e * 2)) & 7) == 0) {
-                    if (pr < Me)
-                        store_row_chunk8<W>(Cb, (long long)pr * ldc_e, tq * BN + c * 32, Ne, f,
-                                            p.out_kind);
+                    store_rows_coalesced8<W>(reinterpret_cast<float*>(sE + (warp - kEpiWarp0) * 4096),
+                                             Cb, ldc_e, prow0 + quarter * 32, Me, tq * BN + c * 32,
+                                             Ne, f, p.out_kind, lane);
                 } else if (!SWAP && p.ndst == 0 && !vec_e) {
                     store_rows_coalesced<W>(reinterpret_cast<float*>(sE + (warp - kEpiWarp0) * 4096),
                                             Cb, ldc_e, prow0 + quarter * 32, Me, tq * BN + c * 32,

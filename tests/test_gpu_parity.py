@@ -210,6 +210,24 @@ def test_batched_attention_scores(d):
             assert np.array_equal(got, want), (d, s, r)
 
 
+@pytest.mark.parametrize("d", [64, 128])
+def test_batched_attention_scores_bf16_unaligned_rows(d):
+    """bf16 S with rows that are not 16-B aligned: s % 8 == 4 (8-B aligned rows: the warp-
+    transposed 8-B store path) and odd s (2-B aligned: the transposed scalar path), every
+    rung; integer inputs, so S equals the round-to-nearest-even of the exact product."""
+    vx = vxmod()
+    p = vx.Plan(0, d, "bf16", "bf16", "nk")
+    batch = 3
+    for s in (12, 100, 196, 257):
+        Q, Kt = synth.gemm_inputs(s, s, d, "bf16", "nk", kind="int", seed=40 + s, batch=batch)
+        want = _round_to(oracle.gemm(Q, Kt, "nk"), "bf16")
+        for r in p.dump()["rungs"]:
+            if not _ok(r, s):
+                continue
+            got, _ = _run(p, Q, Kt, force=(r["rung_id"], r["splits"][-1]))
+            assert np.array_equal(got, want), (d, s, r)
+
+
 def test_batched_attention_full_size_sampled():
     vx = vxmod()
     for d in (64, 128):
@@ -387,6 +405,32 @@ def test_chained_launches_pdl_dependency():
                 torch.cuda.synchronize()
                 got = X[L % 2].cpu().double().numpy()
                 assert np.array_equal(got, want), (M, r, s)
+
+
+@pytest.mark.parametrize("bl", ["nk", "kn"])
+def test_fp32_simt_chained_pdl_exact(bl):
+    """fp32 CUDA-core rungs (2-stage SMEM ring, programmatic dependent launch): a chain of
+    launches where launch i reads what launch i-1 wrote (RAW) and overwrites what it read
+    (WAR), B a permutation, K with a tail (K % 16 != 0) -- every rung, exact."""
+    vx = vxmod()
+    N = K = 100
+    rng = np.random.default_rng(11)
+    perm = rng.permutation(K)
+    Bp = np.zeros((N, K), dtype=np.float32)
+    Bp[np.arange(N), perm] = 1.0
+    B = torch.from_numpy(Bp if bl == "nk" else Bp.T.copy()).cuda()
+    p = vx.Plan(N, K, "fp32", "fp32", bl)
+    for M in (1, 37, 129):
+        A0 = torch.from_numpy(rng.integers(-3, 4, size=(M, K)).astype(np.float32))
+        want = A0.double().numpy()
+        for _ in range(5):
+            want = want[:, perm]
+        for r in p.dump()["rungs"]:
+            X = [A0.cuda(), torch.empty((M, K), dtype=torch.float32, device="cuda")]
+            for i in range(5):
+                p.gemm(X[i % 2], B, out=X[(i + 1) % 2], force=(r["rung_id"], 1))
+            torch.cuda.synchronize()
+            assert np.array_equal(X[5 % 2].cpu().double().numpy(), want), (M, r)
 
 
 def test_gemv_column_tail_nk():
