@@ -22,34 +22,34 @@
 namespace vx {
 
 static const Calib kCalib = {
-    /*hbm_milli=*/3327023,   // 6543 GB/s measured copy bandwidth / 1.965 GHz
+    /*hbm_milli=*/3333028,   // 6543 GB/s measured copy bandwidth / 1.965 GHz
     /*dsm_milli=*/3539,      // effective in-cluster reduce rate (fitted)
-    /*fixed_cluster=*/652,  // cluster launch + two cluster barriers (fitted)
-    /*skfix_milli=*/13315,   // stream-K partial write + read-back (fitted)
-    /*stagger=*/3478,       // first wave > sm_count / 2 CTAs, back to back (R21; fitted)
+    /*fixed_cluster=*/750,  // cluster launch + two cluster barriers (fitted)
+    /*skfix_milli=*/12681,   // stream-K partial write + read-back (fitted)
+    /*stagger=*/3176,       // first wave > sm_count / 2 CTAs, back to back (R21; fitted)
 };
 
 static const RungCalib kRungs[] = {
     {"umma_128x64", 1000367, 46603, 8000, 6919},
-    {"umma_128x128", 1596919, 115222, 12267, 429},
-    {"umma_128x256", 1923790, 160000, 30923, 200},
-    {"umma_256x128", 3611307, 86550, 93781, 3027},
-    {"umma_256x64", 2423501, 160000, 56567, 9724},
-    {"umma_256x256", 4096000, 160000, 77365, 1174},
-    {"umma_swap_128x16", 1000000, 44897, 10901, 4053},
-    {"umma_swap_128x32", 1000000, 43557, 9152, 3404},
-    {"umma_swap_128x64", 1126745, 107013, 10678, 2864},
-    {"umma_swap_128x128", 1597532, 51409, 8000, 788},
+    {"umma_128x128", 1388625, 74650, 15451, 210},
+    {"umma_128x256", 1844329, 160000, 42072, 200},
+    {"umma_256x128", 4351000, 86550, 35705, 3315},
+    {"umma_256x64", 2627000, 160000, 41917, 10210},
+    {"umma_256x256", 5503000, 76190, 50534, 1812},
+    {"umma_swap_128x16", 1656315, 42759, 23878, 4053},
+    {"umma_swap_128x32", 1000000, 43557, 8000, 3404},
+    {"umma_swap_128x64", 1126745, 66468, 10678, 2864},
+    {"umma_swap_128x128", 1458616, 70517, 18400, 827},
     // BN = 192 / swapped BN = 192, 256 (tile-boundary cliffs, R6)
-    {"umma_128x192", 1400000, 160000, 49661, 200},
-    {"umma_swap_128x192", 1738143, 79876, 19110, 507},
-    {"umma_swap_128x256", 1936545, 160000, 27826, 338},
+    {"umma_128x192", 1458056, 160000, 38595, 200},
+    {"umma_swap_128x192", 1587000, 160000, 23619, 200},
+    {"umma_swap_128x256", 2033372, 160000, 23044, 200},
     // TMA-multicast clusters
-    {"umma_mc2_128x128", 1884796, 41151, 39291, 2674},
-    {"umma_mc2_128x256", 4096000, 38348, 512000, 2762},
-    {"umma_swap_mc2_128x32", 1950476, 36460, 8000, 5361},
-    {"umma_swap_mc2_128x64", 1050000, 76964, 38169, 6454},
-    {"umma_swap_mc4_128x64", 2058000, 36408, 512000, 6776},
+    {"umma_mc2_128x128", 1795044, 43276, 24244, 2674},
+    {"umma_mc2_128x256", 4096000, 46305, 28627, 3502},
+    {"umma_swap_mc2_128x32", 1393197, 36460, 8000, 5361},
+    {"umma_swap_mc2_128x64", 1050000, 63738, 40077, 6454},
+    {"umma_swap_mc4_128x64", 1690500, 36408, 512000, 6776},
     {"gemv_1x8", 23780, 9151, 1000, 3332},
     {"gemv_2x8", 8243, 43894, 1000, 3215},
     {"gemv_4x8", 8776, 64524, 1000, 2932},

@@ -286,6 +286,24 @@ def fit(args):
     print(json.dumps(out, indent=1))
 
 
+def measured_pair_mac(raw):
+    """L0 empirical rate of each cta_group::2 pair rung, read off the calibration profile:
+    the best steady-state MACs per (CLOCK_GHZ) cycle per resident pair over the grid shapes
+    with >= 4 waves of pair tiles (the mainloop is then essentially the whole time):
+    M*N*K / (t * clock * pairs)."""
+    pairs = raw["desc"]["max_active_clusters"]["2"]
+    best = {}
+    for sm in raw["samples"]:
+        if sm["bm"] != 256 or sm["split"] != 1 or sm.get("mc", 1) != 1:
+            continue
+        tiles = -(-sm["M"] // 256) * -(-sm["N"] // sm["bn"])
+        if tiles < 4 * pairs:
+            continue
+        rate = sm["M"] * sm["N"] * sm["K"] / (sm["us"] * 1e-6 * CLOCK_GHZ * 1e9 * pairs)
+        best[sm["bn"]] = max(best.get(sm["bn"], 0.0), rate)
+    return {k: round(v) for k, v in best.items()}
+
+
 def fit_fast(args):
     """Same objective and coordinate search as fit(), with per-sample predictions cached: a
     step on one rung's constant re-evaluates only that rung's samples (a global constant
@@ -317,6 +335,14 @@ def fit_fast(args):
         if k[0] == "gemv":
             lo += [math.log(1), math.log(4), math.log(1), math.log(200)]
             hi += [math.log(512), math.log(256), math.log(512), math.log(12000)]
+        elif k[1] == 256 and args.pair_mac:
+            # cta_group::2 pairs: the MMA rate is MEASURED, not fitted -- steady-state MACs
+            # per (1.965 GHz) cycle per pair of the largest calibration shapes, where the
+            # pair's mainloop is the whole time (the fitted value otherwise sits on the
+            # single-SM bound, 4096, i.e. prices a 2-SM tile at one SM's rate)
+            m = args.pair_mac[k[2]] if k[2] in args.pair_mac else 4096
+            lo += [math.log(m), math.log(8), math.log(8), math.log(200)]
+            hi += [math.log(m) + 1e-9, math.log(160), math.log(512), math.log(12000)]
         else:
             lo += [math.log(1000), math.log(8), math.log(8), math.log(200)]
             hi += [math.log(4096), math.log(160), math.log(512), math.log(12000)]
@@ -471,11 +497,19 @@ def main():
     f.add_argument("--seed", type=int, default=0)
     f.add_argument("--fast", action="store_true", help="cached-prediction coordinate search")
     f.add_argument("--out", default=None)
+    f.add_argument("--pair-mac", default=None,
+                   help="'auto' (from the raw profile) or BN:mac,...: measured MAC/cycle per "
+                        "cta_group::2 pair, frozen in the fit")
     h = sub.add_parser("heldout")
     h.add_argument("raw")
     h.add_argument("sweep")
     h.add_argument("calib", nargs="+")
     args = ap.parse_args()
+    if getattr(args, "pair_mac", None) == "auto":
+        args.pair_mac = measured_pair_mac(json.load(open(args.raw)))
+        print("measured pair MAC / cycle:", args.pair_mac, flush=True)
+    elif getattr(args, "pair_mac", None):
+        args.pair_mac = {int(a): float(b) for a, b in (x.split(":") for x in args.pair_mac.split(","))}
     if args.cmd == "measure":
         measure(args)
     elif args.cmd == "heldout":
