@@ -557,6 +557,11 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
             // ===== TMA producers: producer `pid` takes this CTA's k-blocks j % 2 == pid =====
             const int pid = warp == 0 ? 0 : 1;
             const bool kd = p.kdouble && !P_MN && !Q_MN && !p.bpack && MC == 1;
+            // unit ring (deep-K, cta_group::1): the ring is walked in fixed stage pairs, one
+            // barrier round trip per two k-blocks on both sides
+            const bool ur = !PAIR && kd && !(p.dbg & 8192);
+            const int NU = S / 2;            // units in the ring (an odd last stage is unused)
+            int unit = 0;
             const long long cy0 = p.trace ? clock64() : 0;   // trace: setup -> first issue
             const uint64_t pol = (p.dbg & 1024) ? ptx::policy_evict_first()
                                : (p.dbg & 2048) ? ptx::policy_evict_normal()
@@ -604,6 +609,36 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
                 if (p.ngroups) decode_varlen<BN>(tile, p.cu, p.ngroups, tp, tq, vt);
                 else decode_ctile<SWAP, MC>(tile, p.tiles_p, p.tiles_q, crank, b, tp, tq, p.group_p);
                 if (pid == 0 && j == 0) cyc_at(p, 22, cy0);
+                if (ur) {
+                    // unit ring: unit u = stages (2u, 2u+1), one full / one empty barrier
+                    // (the even stage's); a unit carries two k-blocks (one two-chunk box per
+                    // operand) or the range's last odd one (plain boxes into stage 2u)
+                    for (int kb = k0; kb < k0 + nk; kb += 2, ++j) {
+                        const int n2 = k0 + nk - kb >= 2 ? 2 : 1;
+                        if (j % PW != pid) {
+                            if (++unit == NU) { unit = 0; phase ^= 1; }
+                            continue;
+                        }
+                        const int st = 2 * unit;
+                        ptx::mbar_wait(&empty[st], phase ^ 1);
+                        if (j == 0) cyc_at(p, 23, cy0);
+                        if (j < 8) cyc_at(p, 40 + j, cyc_entry);
+                        ptx::mbar_arrive_expect_tx(&full[st], n2 * (kP + kQ));
+                        dep_wait(tile, kb, k0 + nk - kb);
+                        if (!stamped && kb == k0) trace_at(p, 11);
+                        uint8_t* dP = sP + st * kP;
+                        uint8_t* dQ = sQ + st * kQ;
+                        if (n2 == 2) {
+                            ptx::tma_load_4d(dP, &tmP2, &full[st], 0, tp * 128 + vt.row0, kb, b, pol);
+                            ptx::tma_load_4d(dQ, &tmQ2, &full[st], 0, tq * BN + vt.row0, kb, b, pol);
+                        } else {
+                            ptx::tma_load_3d(dP, &tmP, &full[st], kb * 64, tp * 128 + vt.row0, b, pol);
+                            ptx::tma_load_3d(dQ, &tmQ, &full[st], kb * 64, tq * BN + vt.row0, b, pol);
+                        }
+                        if (++unit == NU) { unit = 0; phase ^= 1; }
+                    }
+                    continue;
+                }
                 for (int kb = k0; kb < k0 + nk; ++kb, ++j) {
                     // a unit is one k-block, or two (deep-K) when the next k-block of this
                     // range lands in the next ring stage without a wrap; the MMA issuer walks
@@ -761,6 +796,9 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
             uint32_t phase = 0;
             int it = 0;
             const bool kd = p.kdouble && !P_MN && !Q_MN && !p.bpack && MC == 1;
+            const bool ur = !PAIR && kd && !(p.dbg & 8192);   // unit ring (producers' rule)
+            const int NU = S / 2;
+            int unit = 0;
             WorkIter wi(p, rank);
             int tile, k0, nk;
             for (; wi.next(p, tile, k0, nk); ++it) {
@@ -776,6 +814,41 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
                 // one completion per ring round, so the parity this loop tracks stays exact.
                 // (Per-unit MMA-warp time is what bounds small tiles: DESIGN.md 4.4.)
                 int nunit = 0;   // trace: units of the first tile
+                if (ur) {
+                    for (int i = 0; i < nk; i += 2) {
+                        const int n2 = nk - i >= 2 ? 2 : 1;
+                        const int st = 2 * unit;
+                        const long long c0 = tr ? clock64() : 0;
+                        ptx::mbar_wait(&full[st], phase);
+                        ptx::tc_fence_after();
+                        const long long c1 = tr ? clock64() : 0;
+                        if (it == 0 && i == 0 && lane == 0) trace_at(p, 3);
+                        if (tr && it == 0 && lane == 0 && nunit < 8) cyc_at(p, 48 + nunit, cyc_entry);
+                        ++nunit;
+                        const uint64_t dp0 = dP_base + (uint64_t)(st * (kP >> 4));
+                        const uint64_t dq0 = dQ_base + (uint64_t)(st * (kQ >> 4));
+                        long long c2 = 0;
+                        if (ptx::elect_one()) {
+                            if (!mma_off) {
+#pragma unroll
+                                for (int k = 0; k < 8; ++k) {
+                                    if (k >= 4 && n2 == 1) break;
+                                    const uint64_t dp = dp0 + (k >> 2) * (kP >> 4) + (k & 3) * kStepP;
+                                    const uint64_t dq = dq0 + (k >> 2) * (kQ >> 4) + (k & 3) * kStepQ;
+                                    ptx::umma_f16(d_tmem, dp, dq, idesc, (i | k) != 0);
+                                }
+                            }
+                            c2 = tr ? clock64() : 0;
+                            ptx::umma_commit(&empty[st]);   // frees both stages of the unit
+                            if (tr) {
+                                const long long c3 = clock64();
+                                cyc_wait += c1 - c0; cyc_mma += c2 - c1; cyc_commit += c3 - c2; ++cyc_n;
+                            }
+                        }
+                        __syncwarp();
+                        if (++unit == NU) { unit = 0; phase ^= 1; }
+                    }
+                } else
                 for (int i = 0; i < nk;) {
                     const bool dbl = kd && i + 1 < nk && stage + 1 < S;
                     const long long c0 = tr ? clock64() : 0;
