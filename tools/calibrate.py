@@ -38,7 +38,7 @@ def measure(args):
     import torch
     import paper_2409_01075_b200 as vx
     sys.path.insert(0, os.path.join(ROOT, "tools"))
-    from sweep import time_graph
+    from sweep import graph_buffers, time_graph
     dev = torch.device("cuda", 0)
     stream = torch.cuda.current_stream(dev)
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
@@ -48,16 +48,18 @@ def measure(args):
         p = vx.Plan(N, K, "bf16", "bf16", "nk")
         rungs = p.dump()["rungs"]
         for M in CAL_M:
+            bufs = graph_buffers(1, M, N, K, dev, l2)    # one operand set per shape
             for r in rungs:
                 if r["family"] == 3 and M > r["bm"]:
                     continue
                 for s in r["splits"]:
-                    t = time_graph(p, 1, M, N, K, r["rung_id"], s, dev, stream, l2, 3, "nk")
+                    t = time_graph(p, 1, M, N, K, r["rung_id"], s, dev, stream, l2, 3, "nk", bufs)
                     out["samples"].append({"M": M, "N": N, "K": K, "rung": r["rung_id"],
                                            "family": r["family"], "bm": r["bm"], "bn": r["bn"],
                                            "mc": r.get("mc", 1), "occ": r.get("occ", 1),
                                            "stages": r["stages"],
                                            "split": s, "us": t})
+            del bufs
             print("N=%d K=%d M=%d done" % (N, K, M), flush=True)
     json.dump(out, open(args.out, "w"))
 

@@ -64,14 +64,22 @@ def time_launch(fn, flush, reps, stream):
     return statistics.median(ts)
 
 
-def time_graph(p, batch, M, N, K, r, s, dev, stream, l2_bytes, reps, layout):
-    """Per-launch time of back-to-back launches over rotating buffer sets whose total
-    exceeds 3x L2 (cold operands every launch), captured once in a CUDA graph."""
+def graph_buffers(batch, M, N, K, dev, l2_bytes):
+    """Rotating operand sets for time_graph: R sets whose total exceeds 3x L2."""
     set_bytes = 2 * batch * (M * K + N * K + M * N)
     R = int(min(512, max(4, -(-3 * l2_bytes // set_bytes))))
     A = synth.matrix((R, batch * M * K), "bf16", seed=M, device=dev)
     B = synth.matrix((R, batch * N * K), "bf16", seed=N, scale=K ** -0.5, device=dev)
     C = torch.empty((R, batch * M * N), dtype=torch.bfloat16, device=dev)
+    return A, B, C
+
+
+def time_graph(p, batch, M, N, K, r, s, dev, stream, l2_bytes, reps, layout, bufs=None):
+    """Per-launch time of back-to-back launches over rotating buffer sets whose total
+    exceeds 3x L2 (cold operands every launch), captured once in a CUDA graph.  bufs: the
+    (A, B, C) of graph_buffers, reused across calls for the same shape."""
+    A, B, C = bufs if bufs is not None else graph_buffers(batch, M, N, K, dev, l2_bytes)
+    R = A.shape[0]
     g = torch.cuda.CUDAGraph()
     side = torch.cuda.Stream(dev)
     side.wait_stream(stream)
@@ -100,7 +108,7 @@ def time_graph(p, batch, M, N, K, r, s, dev, stream, l2_bytes, reps, layout):
         e1.record(stream)
         e1.synchronize()
         ts.append(e0.elapsed_time(e1) * 1e3 / R)
-    del g, A, B, C
+    del g
     return statistics.median(ts)
 
 
@@ -140,9 +148,12 @@ def main():
         run(-1, 0)
         l2 = torch.cuda.get_device_properties(dev).L2_cache_size
 
+        bufs = graph_buffers(batch, M, N, K, dev, l2) if args.method == "graph" else None
+
         def timed(r, s):
             if args.method == "graph":
-                return time_graph(p, batch, M, N, K, r, s, dev, stream, l2, args.reps, args.layout)
+                return time_graph(p, batch, M, N, K, r, s, dev, stream, l2, args.reps, args.layout,
+                                  bufs)
             return time_launch(lambda: run(r, s), flush, args.reps, stream)
 
         t_sel = timed(-1, 0)
@@ -168,7 +179,7 @@ def main():
                 entry["best"]["rung"], entry["best"]["split"], entry["best"]["us"],
                 entry["regret"])), flush=True)
         res.append(entry)
-        del A, B, C
+        del A, B, C, bufs
     if args.out:
         json.dump(res, open(args.out, "w"), indent=1)
     if not args.selected_only:
