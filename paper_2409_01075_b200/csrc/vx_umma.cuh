@@ -40,7 +40,11 @@ constexpr int kEpiThreads = kEpiWarps * 32;
 // two halve that and leave the 128xBN tiles MMA- or bandwidth-bound.
 constexpr int kProdWarps = 2;
 constexpr int kProdWarp1 = kEpiWarp0 + kEpiWarps;          // the second producer warp
-constexpr int kThreads = (kEpiWarp0 + kEpiWarps + kProdWarps - 1) * 32;
+// the second MMA issuer (dual-issue mode, DESIGN.md 4.1 "dual MMA issuers"): small-N tiles
+// are paced by one thread's UTCHMMA / commit / wait sequence, so two warps take alternate
+// units of a tile into two TMEM accumulators that the epilogue adds
+constexpr int kMma2Warp = kProdWarp1 + 1;
+constexpr int kThreads = (kMma2Warp + 1) * 32;
 __device__ __forceinline__ bool is_epi_warp(int w) { return w >= kEpiWarp0 && w < kEpiWarp0 + kEpiWarps; }
 
 struct UmmaParams {
@@ -454,6 +458,18 @@ __device__ __forceinline__ void sk_reset(const UmmaParams& p, int c0, int c1, ui
         for (int j = c0; j <= c1; ++j) p.flags[sk_slot<PAIR>(j, rank)] = 0;
 }
 
+// dual MMA issuers: add the second issuer's accumulator (W columns at TMEM address a2) into
+// the W fp32 values (as bits) already loaded from the first one -- fixed order acc0 + acc1
+template <int W>
+__device__ __forceinline__ void acc_add(uint32_t a2, uint32_t* v) {
+    uint32_t w[32];
+    if (W >= 32) ptx::tmem_ld32(a2, w);
+    else ptx::tmem_ld16(a2, w);
+    ptx::tmem_wait_ld();
+#pragma unroll
+    for (int j = 0; j < W; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + __uint_as_float(w[j]));
+}
+
 // SWAP: P = B, Q = A.  P_MN / Q_MN: that operand is MN-major in SMEM (B stored K x N).
 // PAIR: cta_group::2 rung -- a cluster of 2 CTAs computes a 256 x BN tile; each CTA loads
 // its 128 rows of A and BN/2 rows of B, the leader (rank 0) issues the 256-row MMAs, each
@@ -484,6 +500,10 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
     constexpr bool MCQ = MC > 1 && SWAP;    // A = Q is the multicast operand
     constexpr uint16_t kMcMask = (uint16_t)((1u << MC) - 1);
     using Cfg = UmmaCfg<BN>;
+    // dual MMA issuers: cta_group::1, no multicast, BN <= 128 (4 BN TMEM columns: two issuers
+    // x two accumulator buffers)
+    constexpr bool DUALOK = !PAIR && MC == 1 && !LEAN && BN <= 128;
+    constexpr int kCols = DUALOK ? (4 * BN <= 32 ? 32 : 4 * BN) : Cfg::kTmemCols;
     constexpr int kP = Cfg::kPBytes;
     constexpr int kQ = PAIR ? Cfg::kQBytes / 2 : Cfg::kQBytes;   // this CTA's B rows
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -507,6 +527,10 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
     uint8_t* sQ = sP + S * kP;
     uint8_t* sE = sQ + S * kQ;  // epilogue staging: 4 warps x 2 x 4 KB (TMA-store tiles)
 
+    // dual MMA issuers (DUALOK rungs walking the unit ring): warps 1 and kMma2Warp take
+    // alternate units of every tile into accumulators 2 acc and 2 acc + 1 (BN columns each)
+    const bool dual = DUALOK && p.kdouble && !P_MN && !Q_MN && !p.bpack &&
+                      !(p.dbg & 8192) && !(p.dbg & 262144);
     if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&tmP);
         ptx::prefetch_tmap(&tmQ);
@@ -520,7 +544,7 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
             ptx::mbar_init(&empty[i], MC);   // one release per consuming CTA of the cluster
         }
         for (int i = 0; i < 2; ++i) {
-            ptx::mbar_init(&tfull[i], 1);
+            ptx::mbar_init(&tfull[i], dual ? 2 : 1);   // one commit per MMA issuer
             ptx::mbar_init(&tempty[i], PAIR ? 2 * EW : EW);
         }
         ptx::mbar_init(redbar, 1);
@@ -529,8 +553,8 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
     }
     if (warp == 1) {
         const long long c = clock64();
-        if (PAIR) ptx::tmem_alloc_pair<Cfg::kTmemCols>(tmem_holder);
-        else ptx::tmem_alloc<Cfg::kTmemCols>(tmem_holder);
+        if (PAIR) ptx::tmem_alloc_pair<kCols>(tmem_holder);
+        else ptx::tmem_alloc<kCols>(tmem_holder);
         if (lane == 0) cyc_at(p, 28, c);
     }
     ptx::tc_fence_before();
@@ -560,7 +584,11 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
             // unit ring (deep-K, cta_group::1): the ring is walked in fixed stage pairs, one
             // barrier round trip per two k-blocks on both sides
             const bool ur = !PAIR && kd && !(p.dbg & 8192);
-            const int NU = S / 2;            // units in the ring (an odd last stage is unused)
+            // units in the ring (an odd last stage is unused).  With dual issuers the count is
+            // EVEN, so every slot is always consumed by the same issuer: the parity waits on a
+            // slot must never run a round ahead, which an issuer skipping the other's units
+            // could otherwise do on a slot whose rounds alternate between issuers
+            const int NU = dual ? ((S / 2) & ~1) : S / 2;
             int unit = 0;
             const long long cy0 = p.trace ? clock64() : 0;   // trace: setup -> first issue
             const uint64_t pol = (p.dbg & 1024) ? ptx::policy_evict_first()
@@ -776,10 +804,12 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
             }
             if (pid == 0) trace_at(p, 2);
         }
-    } else if (warp == 1) {
+    } else if (warp == 1 || (dual && warp == kMma2Warp)) {
         if (prank == 0) {
             // ===== MMA issuer: the whole warp walks the loop (warp-uniform operands), one
-            // elected lane issues (the pair leader's warp for PAIR rungs) =====
+            // elected lane issues (the pair leader's warp for PAIR rungs); with dual
+            // issuers warp kMma2Warp takes the odd units of every tile =====
+            const int mi = warp == 1 ? 0 : 1;
             long long cyc_wait = 0, cyc_mma = 0, cyc_commit = 0, cyc_n = 0;   // trace only
             const bool tr = p.trace != nullptr;
             const uint32_t idesc = p.idesc;
@@ -797,8 +827,9 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
             int it = 0;
             const bool kd = p.kdouble && !P_MN && !Q_MN && !p.bpack && MC == 1;
             const bool ur = !PAIR && kd && !(p.dbg & 8192);   // unit ring (producers' rule)
-            const int NU = S / 2;
+            const int NU = dual ? ((S / 2) & ~1) : S / 2;   // as the producers
             int unit = 0;
+            long long gu = 0;   // units walked so far (all tiles): issuer = gu % 2
             WorkIter wi(p, rank);
             int tile, k0, nk;
             for (; wi.next(p, tile, k0, nk); ++it) {
@@ -806,7 +837,7 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
                 const uint32_t acc_phase = (it >> 1) & 1;
                 ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
                 ptx::tc_fence_after();
-                const uint32_t d_tmem = tmem_base + acc * BN;
+                const uint32_t d_tmem = tmem_base + (dual ? acc * 2 + mi : acc) * BN;
                 // one iteration per unit: a k-block, or a deep-K pair of k-blocks that landed
                 // together on full[stage] (the producers' rule) -- one wait, 4 or 8 MMAs, one
                 // commit per stage.  The second stage's barrier only got the producer's plain
@@ -815,15 +846,23 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
                 // (Per-unit MMA-warp time is what bounds small tiles: DESIGN.md 4.4.)
                 int nunit = 0;   // trace: units of the first tile
                 if (ur) {
+                    int myk = 0;   // k-blocks this issuer has accumulated in this tile
                     for (int i = 0; i < nk; i += 2) {
                         const int n2 = nk - i >= 2 ? 2 : 1;
                         const int st = 2 * unit;
+                        // the issuer of a unit is the parity of its GLOBAL index, so with an
+                        // even NU every ring slot always has the same issuer
+                        if (dual && (int)(gu++ & 1) != mi) {   // the other issuer's unit
+                            if (++unit == NU) { unit = 0; phase ^= 1; }
+                            continue;
+                        }
                         const long long c0 = tr ? clock64() : 0;
                         ptx::mbar_wait(&full[st], phase);
                         ptx::tc_fence_after();
                         const long long c1 = tr ? clock64() : 0;
-                        if (it == 0 && i == 0 && lane == 0) trace_at(p, 3);
-                        if (tr && it == 0 && lane == 0 && nunit < 8) cyc_at(p, 48 + nunit, cyc_entry);
+                        if (it == 0 && i == 0 && lane == 0 && mi == 0) trace_at(p, 3);
+                        if (tr && it == 0 && lane == 0 && mi == 0 && nunit < 8)
+                            cyc_at(p, 48 + nunit, cyc_entry);
                         ++nunit;
                         const uint64_t dp0 = dP_base + (uint64_t)(st * (kP >> 4));
                         const uint64_t dq0 = dQ_base + (uint64_t)(st * (kQ >> 4));
@@ -835,7 +874,7 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
                                     if (k >= 4 && n2 == 1) break;
                                     const uint64_t dp = dp0 + (k >> 2) * (kP >> 4) + (k & 3) * kStepP;
                                     const uint64_t dq = dq0 + (k >> 2) * (kQ >> 4) + (k & 3) * kStepQ;
-                                    ptx::umma_f16(d_tmem, dp, dq, idesc, (i | k) != 0);
+                                    ptx::umma_f16(d_tmem, dp, dq, idesc, (myk | k) != 0);
                                 }
                             }
                             c2 = tr ? clock64() : 0;
@@ -846,6 +885,8 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
                             }
                         }
                         __syncwarp();
+                        if (!dual) ++gu;
+                        myk += n2;
                         if (++unit == NU) { unit = 0; phase ^= 1; }
                     }
                 } else
@@ -903,7 +944,7 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
                 }
                 __syncwarp();
             }
-            if (lane == 0) {
+            if (lane == 0 && mi == 0) {
                 trace_at(p, 4);
                 if (tr) {
                     p.trace[blockIdx.x * kTraceSlots + 12] = cyc_wait;
@@ -929,6 +970,7 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
             else ptx::mbar_arrive(bar);
         };
         int it = 0;
+        long long gue = 0;   // dual issuers: units of the tiles before this one (MMA's gu)
         WorkIter wi(p, rank);
         int tile, k0, nk;
         const long long U = (long long)p.num_tiles * p.kb_total;
@@ -979,7 +1021,15 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
             const bool st0 = it == 0 && threadIdx.x == kEpiWarp0 * 32;
             const long long cye = st0 ? clock64() : 0;
             if (st0) trace_at(p, 5);
-            const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
+            // dual issuers: accumulator 2 acc holds this tile's even-indexed units (global unit
+            // count), 2 acc + 1 (BN columns further) the odd ones; a one-unit range fills only
+            // the one its parity names
+            const long long u0 = gue;
+            gue += (nk + 1) / 2;
+            const bool has0 = !dual || nk >= 3 || (u0 & 1) == 0;
+            const bool two = dual && nk >= 3;
+            const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) +
+                                   (dual ? acc * 2 + (has0 ? 0 : 1) : acc) * BN;
             if (split) break;  // split mode: the accumulator is read after the cluster barrier
             // ---- stream-K: a cut tile ----------------------------------------------------
             if (p.streamk && k0 > 0 && !(p.dbg & 32)) {
@@ -993,6 +1043,7 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
                     else ptx::tmem_ld16(taddr + c * 32, v);
                     ptx::tmem_wait_ld();
                     constexpr int W = BN >= 32 ? 32 : BN;
+                    if (two) acc_add<W>(taddr + BN + c * 32, v);
 #pragma unroll
                     for (int j = 0; j < W; j += 4)
                         __stcg(reinterpret_cast<uint4*>(slot + (long long)((c * 32 + j) / 4) * 128 * 4),
@@ -1028,6 +1079,7 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
                             uint32_t v[32];
                             ptx::tmem_ld32(taddr + k * CW, v);
                             ptx::tmem_wait_ld();
+                            if (two) acc_add<32>(taddr + BN + k * CW, v);
                             add_partials<32, PAIR>(v, p.ws, c_first, c_last, row, k * CW, BN, prank);
 #pragma unroll
                             for (int j = 0; j < 8; ++j)
@@ -1039,6 +1091,10 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
                             ptx::tmem_ld32(taddr + k * CW + 32,
                                            *reinterpret_cast<uint32_t(*)[32]>(v + 32));
                             ptx::tmem_wait_ld();
+                            if (two) {
+                                acc_add<32>(taddr + BN + k * CW, v);
+                                acc_add<32>(taddr + BN + k * CW + 32, v + 32);
+                            }
                             if (st0 && k == grp) cyc_at(p, 29, cye);
                             add_partials<64, PAIR>(v, p.ws, c_first, c_last, row, k * CW, BN, prank);
                             uint32_t u[32];
@@ -1069,6 +1125,7 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
                         if (BN >= 32) ptx::tmem_ld32(taddr + c * 32, v);
                         else ptx::tmem_ld16(taddr + c * 32, v);
                         ptx::tmem_wait_ld();
+                        if (two) acc_add<W>(taddr + BN + c * 32, v);
                         add_partials<W, PAIR>(v, p.ws, c_first, c_last, row, c * 32, BN, prank);
                         const float* f = reinterpret_cast<const float*>(v);
                         // staging tile [W m-rows][32 n] (row pitch 32*ob bytes), lane = n
@@ -1120,6 +1177,7 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
                 else ptx::tmem_ld16(taddr + c * 32, v);
                 ptx::tmem_wait_ld();
                 constexpr int W = BN >= 32 ? 32 : BN;
+                if (two) acc_add<W>(taddr + BN + c * 32, v);
                 add_partials<W, PAIR>(v, p.ws, c_first, c_last, row, c * 32, BN, prank);
                 const float* f = reinterpret_cast<const float*>(v);
                 if (p.dbg & 8) {
@@ -1212,6 +1270,7 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
             const uint32_t dst = owner == rank ? base : ptx::mapa(base, owner);
             const uint32_t rbar = ptx::mapa(ptx::smem_addr(redbar), owner);
             const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16);
+            const bool two = dual && p.kb_total / s_ >= 3;   // this slice's units >= 2
             const int grp = (warp - kEpiWarp0) >> 2;
             const int sw = G == 8 ? (rr & 7) : G == 4 ? ((rr >> 1) & 3) : 0;
 #pragma unroll 1
@@ -1220,6 +1279,7 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
                 if (BN >= 32) ptx::tmem_ld32(taddr + c * 32, v);
                 else ptx::tmem_ld16(taddr + c * 32, v);
                 ptx::tmem_wait_ld();
+                if (two) acc_add<W>(taddr + BN + c * 32, v);
                 const uint32_t cd = dst + (uint32_t)(c * rows * W) * 4u;
 #pragma unroll
                 for (int g = 0; g < G; ++g) {
@@ -1294,8 +1354,8 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
     if (warp == 1) {
         __syncwarp();
         ptx::tc_fence_after();
-        if (PAIR) ptx::tmem_dealloc_pair<Cfg::kTmemCols>(tmem_base);
-        else ptx::tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+        if (PAIR) ptx::tmem_dealloc_pair<kCols>(tmem_base);
+        else ptx::tmem_dealloc<kCols>(tmem_base);
         if (lane == 0) trace_at(p, 9);
     }
 }

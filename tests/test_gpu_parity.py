@@ -88,6 +88,26 @@ def test_deep_k_units_odd_kblock_counts():
                 assert np.array_equal(got, want), (M, r["rung_id"], s)
 
 
+@pytest.mark.parametrize("K", [128, 192, 320])
+def test_short_k_unit_ring_and_dual_issuers(K):
+    """K = 2, 3, 5 k-blocks: every tile's k-range is 1..3 units of the unit ring, so the
+    second MMA issuer has no unit (2 k-blocks), one full unit (3: 2 + 1) or a half unit, and
+    split / stream-K slices are shorter still -- the epilogue must add the second accumulator
+    exactly when it was written; every rung x split, integer-exact."""
+    vx = vxmod()
+    N = 256
+    p = vx.Plan(N, K, "bf16", "fp32", "nk")
+    for M in (1, 40, 129):
+        A, B = synth.gemm_inputs(M, N, K, "bf16", "nk", kind="int", seed=60 + M + K)
+        want = oracle.gemm(A, B, "nk")
+        for r in p.dump()["rungs"]:
+            if not _ok(r, M):
+                continue
+            for s in r["splits"]:
+                got, _ = _run(p, A, B, force=(r["rung_id"], s))
+                assert np.array_equal(got, want), (K, M, r["rung_id"], s)
+
+
 def test_fp16_inputs_integer_exact():
     vx = vxmod()
     N, K = 256, 320                       # K not a multiple of 64: TMA zero-fills the K tail
