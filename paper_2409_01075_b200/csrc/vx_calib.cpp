@@ -23,37 +23,37 @@ namespace vx {
 
 static const Calib kCalib = {
     /*hbm_milli=*/3333028,   // 6543 GB/s measured copy bandwidth / 1.965 GHz
-    /*dsm_milli=*/3539,      // effective in-cluster reduce rate (fitted)
-    /*fixed_cluster=*/750,  // cluster launch + two cluster barriers (fitted)
-    /*skfix_milli=*/12681,   // stream-K partial write + read-back (fitted)
-    /*stagger=*/3176,       // first wave > sm_count / 2 CTAs, back to back (R21; fitted)
+    /*dsm_milli=*/3077,      // effective in-cluster reduce rate (fitted)
+    /*fixed_cluster=*/1125,  // cluster launch + two cluster barriers (fitted)
+    /*skfix_milli=*/10417,   // stream-K partial write + read-back (fitted)
+    /*stagger=*/1134,       // first wave > sm_count / 2 CTAs, back to back (R21; fitted)
 };
 
 static const RungCalib kRungs[] = {
-    {"umma_128x64", 1000367, 46603, 8000, 6919},
-    {"umma_128x128", 1388625, 74650, 15451, 210},
-    {"umma_128x256", 1844329, 160000, 42072, 200},
-    {"umma_256x128", 4351000, 86550, 35705, 3315},
-    {"umma_256x64", 2627000, 160000, 41917, 10210},
-    {"umma_256x256", 5503000, 76190, 50534, 1812},
-    {"umma_swap_128x16", 1656315, 42759, 23878, 4053},
-    {"umma_swap_128x32", 1000000, 43557, 8000, 3404},
-    {"umma_swap_128x64", 1126745, 66468, 10678, 2864},
-    {"umma_swap_128x128", 1458616, 70517, 18400, 827},
+    {"umma_128x64", 1000367, 46985, 8000, 3789},
+    {"umma_128x128", 1259524, 160000, 11200, 294},
+    {"umma_128x256", 1844329, 160000, 33183, 200},
+    {"umma_256x128", 4474000, 82429, 31048, 3315},
+    {"umma_256x64", 3012000, 160000, 512000, 10210},
+    {"umma_256x256", 5385000, 76190, 50534, 1726},
+    {"umma_swap_128x16", 1558204, 44897, 33887, 4053},
+    {"umma_swap_128x32", 2208420, 50091, 8000, 3404},
+    {"umma_swap_128x64", 1183082, 57798, 10678, 2864},
+    {"umma_swap_128x128", 1322500, 71482, 8000, 864},
     // BN = 192 / swapped BN = 192, 256 (tile-boundary cliffs, R6)
-    {"umma_128x192", 1458056, 160000, 38595, 200},
-    {"umma_swap_128x192", 1587000, 160000, 23619, 200},
+    {"umma_128x192", 1331269, 160000, 48934, 200},
+    {"umma_swap_128x192", 1587000, 84000, 22494, 307},
     {"umma_swap_128x256", 2033372, 160000, 23044, 200},
     // TMA-multicast clusters
-    {"umma_mc2_128x128", 1795044, 43276, 24244, 2674},
-    {"umma_mc2_128x256", 4096000, 46305, 28627, 3502},
-    {"umma_swap_mc2_128x32", 1393197, 36460, 8000, 5361},
-    {"umma_swap_mc2_128x64", 1050000, 63738, 40077, 6454},
-    {"umma_swap_mc4_128x64", 1690500, 36408, 512000, 6776},
+    {"umma_mc2_128x128", 1560908, 37631, 34918, 2808},
+    {"umma_mc2_128x256", 2048000, 51051, 40896, 3502},
+    {"umma_swap_mc2_128x32", 1000000, 34724, 9200, 5629},
+    {"umma_swap_mc2_128x64", 1000000, 43359, 512000, 6454},
+    {"umma_swap_mc4_128x64", 1000000, 36408, 512000, 6453},
     {"gemv_1x8", 23780, 9151, 1000, 3332},
     {"gemv_2x8", 8243, 43894, 1000, 3215},
-    {"gemv_4x8", 8776, 64524, 1000, 2932},
-    {"gemv_8x8", 10157, 5087, 148392, 497},
+    {"gemv_4x8", 9612, 64524, 1000, 3079},
+    {"gemv_8x8", 10157, 5087, 148392, 544},
     {"simt_32x32", 128000, 32000, 16000, 2000},
     {"simt_64x64", 128000, 32000, 16000, 2000},
     {"simt_128x64", 128000, 32000, 16000, 2000},
