@@ -31,22 +31,22 @@ static const Calib kCalib = {
 
 static const RungCalib kRungs[] = {
     {"umma_128x64", 1000367, 46985, 8000, 3789},
-    {"umma_128x128", 1259524, 160000, 11200, 294},
-    {"umma_128x256", 1844329, 160000, 33183, 200},
-    {"umma_256x128", 4474000, 82429, 31048, 3315},
+    {"umma_128x128", 1379479, 160000, 11200, 294},
+    {"umma_128x256", 1936545, 160000, 23702, 200},
+    {"umma_256x128", 4474000, 86550, 25883, 4029},
     {"umma_256x64", 3012000, 160000, 512000, 10210},
-    {"umma_256x256", 5385000, 76190, 50534, 1726},
+    {"umma_256x256", 5385000, 80000, 39533, 1359},
     {"umma_swap_128x16", 1558204, 44897, 33887, 4053},
     {"umma_swap_128x32", 2208420, 50091, 8000, 3404},
     {"umma_swap_128x64", 1183082, 57798, 10678, 2864},
-    {"umma_swap_128x128", 1322500, 71482, 8000, 864},
+    {"umma_swap_128x128", 1690500, 124317, 9200, 994},
     // BN = 192 / swapped BN = 192, 256 (tile-boundary cliffs, R6)
-    {"umma_128x192", 1331269, 160000, 48934, 200},
-    {"umma_swap_128x192", 1587000, 84000, 22494, 307},
-    {"umma_swap_128x256", 2033372, 160000, 23044, 200},
+    {"umma_128x192", 1331269, 160000, 59088, 200},
+    {"umma_swap_128x192", 1587000, 80000, 21423, 200},
+    {"umma_swap_128x256", 2135041, 160000, 19906, 200},
     // TMA-multicast clusters
-    {"umma_mc2_128x128", 1560908, 37631, 34918, 2808},
-    {"umma_mc2_128x256", 2048000, 51051, 40896, 3502},
+    {"umma_mc2_128x128", 1939016, 40649, 9200, 2808},
+    {"umma_mc2_128x256", 2048000, 160000, 30470, 3502},
     {"umma_swap_mc2_128x32", 1000000, 34724, 9200, 5629},
     {"umma_swap_mc2_128x64", 1000000, 43359, 512000, 6454},
     {"umma_swap_mc4_128x64", 1000000, 36408, 512000, 6453},

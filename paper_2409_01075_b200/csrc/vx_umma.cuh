@@ -500,9 +500,12 @@ __global__ void __launch_bounds__(LEAN ? 192 : kThreads, LEAN ? 2 : 1)
     constexpr bool MCQ = MC > 1 && SWAP;    // A = Q is the multicast operand
     constexpr uint16_t kMcMask = (uint16_t)((1u << MC) - 1);
     using Cfg = UmmaCfg<BN>;
-    // dual MMA issuers: cta_group::1, no multicast, BN <= 128 (4 BN TMEM columns: two issuers
-    // x two accumulator buffers)
-    constexpr bool DUALOK = !PAIR && MC == 1 && !LEAN && BN <= 128;
+    // dual MMA issuers: cta_group::1, no multicast, BN <= 64 (4 BN TMEM columns: two issuers
+    // x two accumulator buffers).  Not for BN = 128: a 128 x 128 x 16 MMA already keeps the
+    // tensor pipe busy ~2x its issue time, so a second issuer gains nothing while the epilogue
+    // reads twice the TMEM (measured A/B over 7 shapes x every schedule: BN 16 / 32 / 64
+    // x1.12 / x1.08 / x1.05, BN 128 x0.91; tools/dual_ab.py)
+    constexpr bool DUALOK = !PAIR && MC == 1 && !LEAN && BN <= 64;
     constexpr int kCols = DUALOK ? (4 * BN <= 32 ? 32 : 4 * BN) : Cfg::kTmemCols;
     constexpr int kP = Cfg::kPBytes;
     constexpr int kQ = PAIR ? Cfg::kQBytes / 2 : Cfg::kQBytes;   // this CTA's B rows

@@ -44,9 +44,13 @@ def measure(args):
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     out = {"desc": vx.device_probe(0).to_json(), "clock_ghz": CLOCK_GHZ, "samples": []}
     nk_list = CAL_NK[13:] if getattr(args, "only_new", False) else CAL_NK
+    only = set(args.only_keys.split(",")) if getattr(args, "only_keys", None) else None
+    fam_of = {0: "umma", 1: "umma_swap", 3: "gemv"}
     for N, K in nk_list:
         p = vx.Plan(N, K, "bf16", "bf16", "nk")
-        rungs = p.dump()["rungs"]
+        rungs = [r for r in p.dump()["rungs"]
+                 if only is None or calib_key(fam_of[r["family"]], r["bm"], r["bn"], r.get("mc", 1),
+                                              r.get("occ", 1)) in only]
         for M in CAL_M:
             bufs = graph_buffers(1, M, N, K, dev, l2)    # one operand set per shape
             for r in rungs:
@@ -488,6 +492,12 @@ def main():
     m = sub.add_parser("measure")
     m.add_argument("--out", default="gpurun_out/calib_raw.json")
     m.add_argument("--only-new", action="store_true", help="only the round-2 additions to CAL_NK")
+    m.add_argument("--only-keys", default=None,
+                   help="comma-separated calibration keys: re-measure only these rungs")
+    mg = sub.add_parser("merge")
+    mg.add_argument("raw")
+    mg.add_argument("patch")
+    mg.add_argument("--out", required=True)
     f = sub.add_parser("fit")
     f.add_argument("raw")
     f.add_argument("--regret-weight", type=float, default=2.0)
@@ -514,6 +524,15 @@ def main():
         args.pair_mac = {int(a): float(b) for a, b in (x.split(":") for x in args.pair_mac.split(","))}
     if args.cmd == "measure":
         measure(args)
+    elif args.cmd == "merge":
+        # replace the samples of the rungs re-measured in `patch` (same grid) in `raw`
+        raw, patch = json.load(open(args.raw)), json.load(open(args.patch))
+        fam = {0: "umma", 1: "umma_swap", 3: "gemv"}
+        key = lambda x: calib_key(fam[x["family"]], x["bm"], x["bn"], x.get("mc", 1), x.get("occ", 1))
+        redo = {key(x) for x in patch["samples"]}
+        raw["samples"] = [x for x in raw["samples"] if key(x) not in redo] + patch["samples"]
+        json.dump(raw, open(args.out, "w"))
+        print("merged %d re-measured rung keys: %s" % (len(redo), sorted(redo)))
     elif args.cmd == "heldout":
         heldout(args)
     elif args.fast:
