@@ -939,7 +939,10 @@ def load_traffic(dom):
         return d[key]
     # the same (N, K) captured at an M within 0.1% (e.g. 16384 for a dominant M = 16383)
     for k, v in d.items():
-        m, n, kk = (int(x) for x in k.split("_"))
+        parts = k.split("_")
+        if len(parts) != 3 or not all(x.isdigit() for x in parts) or not isinstance(v, int):
+            continue   # bookkeeping keys such as "_round2"
+        m, n, kk = (int(x) for x in parts)
         if n == dom["N"] and kk == dom["K"] and abs(m - dom["M"]) <= 0.001 * dom["M"]:
             return v
     return None
