@@ -378,28 +378,33 @@ __device__ __forceinline__ void store_rows_coalesced(float* st, char* Cb, long l
 }
 
 // 16-bit rows that are 8-B but not 16-B aligned (N % 8 == 4, e.g. attention s = 100, 1500):
-// the warp transposes its 32 rows x W columns through its staging buffer as above, then each
-// store instruction covers 4 rows x 32 columns with one 8-B (4-column) store per lane, so a
-// row's W columns leave as one contiguous 64-B segment -- instead of 32 lanes each writing 8 B
-// into 32 different rows (N % 4 == 0: 4 columns are all-or-nothing)
+// the lane (= tile row) packs its W columns to 16 bit and writes them to row `lane` of a
+// [32 rows][64 B] staging tile as 16-B vectors (granule g of row r at g ^ ((r >> 1) & 3):
+// conflict-free both ways); then each store instruction covers 4 rows x 32 columns, one
+// 8-B shared load + one 8-B global store per lane, so a row's W columns leave as one
+// contiguous 64-B segment (N % 4 == 0: 4 columns are all-or-nothing)
 template <int W>
 __device__ __forceinline__ void store_rows_coalesced8(float* st, char* Cb, long long ldc, int row0,
                                                       int M, int n0, int N, const float* f,
                                                       int kind, int lane) {
+    uint32_t u[W / 2];
+    pack_chunk<W>(f, u, kind);
+    const uint32_t sb = ptx::smem_addr(st);
 #pragma unroll
-    for (int j = 0; j < W; ++j) st[lane * 32 + (j ^ lane)] = f[j];
+    for (int g = 0; g < W / 8; ++g)
+        ptx::st_shared_v4(sb + (uint32_t)lane * 64u + ((uint32_t)(g ^ ((lane >> 1) & 3)) << 4),
+                          u[4 * g], u[4 * g + 1], u[4 * g + 2], u[4 * g + 3]);
     __syncwarp();
     const int c = (lane & 7) * 4;
+    const uint32_t coff = (uint32_t)(c & 4) * 2u;          // byte offset inside the granule
 #pragma unroll 1
     for (int it = 0; it < 8; ++it) {
         const int r = it * 4 + (lane >> 3);
         const int row = row0 + r;
         if (row < M && c < W && n0 + c < N) {
-            const float* sr = st + r * 32;
-            const uint32_t lo = pack2(sr[c ^ r], sr[(c + 1) ^ r], kind);
-            const uint32_t hi = pack2(sr[(c + 2) ^ r], sr[(c + 3) ^ r], kind);
-            *reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(Cb) + (long long)row * ldc + n0 + c) =
-                make_uint2(lo, hi);
+            const uint2 v = ptx::ld_shared_v2(sb + (uint32_t)r * 64u +
+                                              ((uint32_t)((c >> 3) ^ ((r >> 1) & 3)) << 4) + coff);
+            *reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(Cb) + (long long)row * ldc + n0 + c) = v;
         }
     }
     __syncwarp();
