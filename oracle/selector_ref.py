@@ -413,7 +413,8 @@ def _streamk_cost(rung, batch, M, N, K, mt, nt, tm, tn, tiles, kb, in_b, out_b, 
     work units evenly in one wave (Eq. 3 gives F = 1); each CTA's temporal loop is
     ceil(U/G) k-blocks (Eq. 2) touching at most ceil(units/kb)+1 tile segments, whose
     epilogues overlap the loop except the last; a cut tile is completed by adding
-    ceil(kb/units) partials, each one fp32 tile written and read back."""
+    ceil(kb/units) partials, each one fp32 tile (per CTA: its bm/cg rows) written and read
+    back."""
     bm, bn, bk = rung["bm"], rung["bn"], rung["bk"]
     hbm = calib["hbm_milli"]
     U = tiles * kb
@@ -427,7 +428,9 @@ def _streamk_cost(rung, batch, M, N, K, mt, nt, tm, tn, tiles, kb, in_b, out_b, 
     tl = max(l_smem, l_hbm)
     t_main = temporal_cost(tl, units, inner, 0)
     st = max(t_load(bm * bn * out_b, cal["epi_milli"]), t_load(out_b * batch * M * N, segs * hbm))
-    fix = ceil_div(kb, units) * t_load(2 * bm * bn * 4, calib["skfix_milli"])
+    # each CTA finishes its own rows of a cut tile: a pair's CTAs each write and read back
+    # their (bm / cg) x bn fp32 half, in parallel (R19)
+    fix = ceil_div(kb, units) * t_load(2 * (bm // cg) * bn * 4, calib["skfix_milli"])
     cost = max(t_main, segs * st) + st + fix + cal["fixed"]
     if G * cg > desc["sm_count"] // 2:               # R21 (see rung_cost)
         cost += calib["stagger"]

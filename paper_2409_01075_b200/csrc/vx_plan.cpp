@@ -301,8 +301,9 @@ static void rung_cost(const vx_plan_s* p, const Rung& r, int s, int64_t batch, i
         const int64_t tm_ = eq2(tl, units, inner, 0);
         const int64_t st = std::max(t_move(bm * bn * out_b, r.epi_milli),
                                     t_move((int64_t)out_b * batch * M * N, segs * cal.hbm_milli));
-        // a cut tile is finished by adding ceil(kb/units) partials (one write + read each)
-        const int64_t fix = cdiv(kb, units) * t_move(2 * bm * bn * 4, cal.skfix_milli);
+        // a cut tile is finished by adding ceil(kb/units) partials (one write + read each);
+        // every CTA handles its own rows (a pair's two CTAs their bm/2-row halves, in parallel)
+        const int64_t fix = cdiv(kb, units) * t_move(2 * (bm / r.cg) * bn * 4, cal.skfix_milli);
         o->rung_id = r.rung_id; o->split = 0; o->family = r.family; o->swap = r.swap;
         o->bm = r.bm; o->bn = r.bn; o->stages = r.stages;
         o->tiles_m = (int32_t)tm; o->tiles_n = (int32_t)tn; o->grid = (int32_t)(G * r.cg);

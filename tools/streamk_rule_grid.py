@@ -52,7 +52,7 @@ def main():
         l = max(ls, t(2 * K * (mt + nt), units * hbm))
         tm_ = l + (units - 1) * max(l, c) + c
         st = max(t(bm * bn * 2, epi), t(2 * M * N, segs * hbm))
-        cyc = max(tm_, segs * st) + st + C._cd(kb, units) * t(2 * bm * bn * 4, skfix) + fixed
+        cyc = max(tm_, segs * st) + st + C._cd(kb, units) * t(2 * (bm // cgk) * bn * 4, skfix) + fixed
         if G * cgk > desc["sm_count"] // 2:
             cyc += int(round(g["stagger"]))
         waves = tiles * cgk / (desc["max_active_clusters"][str(cgk)] * cgk)
